@@ -1,0 +1,175 @@
+/*
+ * rasterbound_b200.h -- C-ABI of the B200-native epsilon-bounded
+ * point-polygon aggregation engine (librasterbound_b200.so).
+ *
+ * The reference (`rasterbound`, SPEC.md) is a Python package with no FFI; this
+ * header is the boundary its Python API (rasterbound.{grid,raster,act,query})
+ * binds through ctypes (INTEGRATION.md shows the binding).  Each entry point
+ * names the reference operation it replaces.
+ *
+ * Conventions
+ *  - Plain C types only; no exceptions cross the boundary.  Every function
+ *    returns an rb status; rb_last_error() gives a thread-local message.
+ *  - Status codes map 1:1 onto /root/reference/pkg/src/rasterbound/errors.py.
+ *  - "device" pointers are CUDA global-memory pointers (e.g. torch tensors);
+ *    "host" pointers are ordinary CPU memory.  `stream` is a cudaStream_t
+ *    (NULL = legacy default stream).  rb_point_pass / rb_lookup are
+ *    stream-ordered and never synchronise the host.
+ *  - An rb_approx is immutable after rb_approx_build returns; concurrent
+ *    rb_point_pass / rb_lookup calls on one handle are safe.
+ */
+#ifndef RASTERBOUND_B200_H
+#define RASTERBOUND_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes (errors.py:8-37) */
+#define RB_OK 0
+#define RB_GEOMETRY_ERROR (-1)        /* errors.py:12 GeometryError */
+#define RB_DOMAIN_ERROR (-2)          /* errors.py:16 DomainError */
+#define RB_CAPACITY_ERROR (-3)        /* errors.py:20 CapacityError */
+#define RB_CONFIG_ERROR (-4)          /* errors.py:24 ConfigError */
+#define RB_SCHEMA_ERROR (-5)          /* errors.py:28 SchemaError */
+#define RB_SHAPE_ERROR (-6)           /* errors.py:32 ShapeError */
+#define RB_UNSUPPORTED_TRANSFORM (-7) /* errors.py:36 UnsupportedTransform */
+#define RB_CUDA_ERROR (-100)          /* device / driver failure */
+
+/* RasterMode */
+#define RB_MODE_CONSERVATIVE 0
+#define RB_MODE_CENTER_SAMPLED 1
+
+/* cell-index layouts (north star subsystem 2) */
+#define RB_LAYOUT_DENSE 0 /* dense leaf grid of owner values (uniform raster)   */
+#define RB_LAYOUT_TRIE 1  /* multi-level radix table (ACT, hierarchical raster) */
+
+/* point coordinate storage */
+#define RB_XY_F64 0 /* interleaved float64 (x,y) */
+#define RB_XY_F32 1 /* interleaved float32 (x,y), promoted exactly to float64 */
+
+/* owner-value encoding returned by rb_lookup (one uint32 per point):
+ *   0                       no owner
+ *   v in [1, 2^30)          single owner: region = (v-1)>>1, boundary = (v-1)&1
+ *   RB_VALUE_LIST | off     several owners: pool[off] = k, pool[off+1..k] = (region<<1)|boundary */
+#define RB_VALUE_LIST 0x40000000u
+#define RB_VALUE_PAYLOAD 0x3fffffffu
+
+/* GridConfig */
+typedef struct rb_grid {
+  double origin_x, origin_y;
+  double extent;     /* side of the square domain */
+  int32_t max_level; /* L in [0, 31] */
+} rb_grid;
+
+/* Polygon set in CSR form (device pointers).  Ring 0 of every polygon is the
+ * outer ring, further rings are holes; a region may own
+ * several polygons (multi-polygon). */
+typedef struct rb_polygons {
+  const double* vx;
+  const double* vy;
+  int64_t n_vertices;
+  const int64_t* ring_off; /* [n_rings+1] vertex offsets */
+  int64_t n_rings;
+  const int64_t* poly_ring_off; /* [n_polygons+1] ring offsets */
+  int64_t n_polygons;
+  const int32_t* poly_region; /* [n_polygons] region index in [0, n_regions) */
+  int32_t n_regions;
+} rb_polygons;
+
+typedef struct rb_build_opts {
+  int32_t mode;        /* RB_MODE_* */
+  int32_t layout;      /* RB_LAYOUT_* */
+  int32_t radix_width; /* ACT bits per node: 2, 4, 8; default 8 */
+  int32_t root_level;  /* TRIE root table level; -1 = automatic */
+  int32_t keep_cells;  /* keep per-polygon covering cells for export */
+} rb_build_opts;
+
+typedef struct rb_stats {
+  int64_t n_partial_leaves;   /* (polygon, leaf) pairs whose open leaf meets the boundary */
+  int64_t n_interior_cells;   /* hierarchical interior cells over all polygons */
+  int64_t n_boundary_cells;   /* kept boundary leaves over all polygons */
+  int64_t n_uniform_interior; /* interior leaves after expansion to level L */
+  int64_t n_positions;        /* disjoint indexed cells after overlay */
+  int64_t n_multi_owner;      /* positions with more than one owner */
+  int64_t n_nodes;            /* TRIE nodes below the root table */
+  int64_t index_bytes;        /* root + nodes + owner pool */
+  int32_t root_level;
+  int32_t node_levels; /* quad levels per node (radix_width / 2) */
+  int32_t n_regions;
+  int32_t max_level;
+  double build_ms;
+} rb_stats;
+
+typedef struct rb_approx rb_approx;
+
+int32_t rb_version(void);
+const char* rb_last_error(void);
+
+/* grid.level_for_bound */
+int rb_level_for_bound(double extent, double epsilon, int32_t* level_out);
+
+/* raster.rasterize_hierarchical/uniform for a region set + act.act_build
+ * (SPEC.md:216-233, 276-284).  Synchronises `stream` (sizes come back to the
+ * host).  Errors: GeometryError (ring < 3 vertices, NaN, zero area),
+ * DomainError (vertex outside the domain), CapacityError, ConfigError. */
+int rb_approx_build(const rb_grid* grid, const rb_polygons* polys, const rb_build_opts* opts, void* stream,
+                    rb_approx** out);
+/* act.act_build from explicit coverings: device arrays of
+ * n_cells cells (covering index, level <= L, Z code at that level, kind
+ * 1 = interior / 2 = boundary); covering c belongs to region cov_region[c].
+ * Duplicate cells are idempotent (set semantics). */
+int rb_index_from_cells(const rb_grid* grid, int64_t n_cells, const int32_t* cov, const uint8_t* level,
+                        const uint64_t* code, const uint8_t* kind, const int32_t* cov_region, int64_t n_cov,
+                        int32_t n_regions, const rb_build_opts* opts, void* stream, rb_approx** out);
+int rb_approx_stats(const rb_approx* a, rb_stats* out);
+void rb_approx_free(rb_approx* a);
+
+/* query.join_act point loop: per region alpha/beta COUNT and
+ * SUM over n points.  cnt_out: device int64 [n_regions*2] (alpha, beta);
+ * sum_out: device float64 [n_regions*2]; attr: device float32 [n] or NULL.
+ * accumulate=0 overwrites the outputs, 1 adds to them.  first_bad: device
+ * int64 [1], set to the smallest out-of-domain / NaN point index (or left at
+ * INT64_MAX); the caller raises DomainError.  Never syncs. */
+int rb_point_pass(const rb_approx* a, const void* xy, int32_t xy_dtype, int64_t n, const float* attr,
+                  int64_t* cnt_out, double* sum_out, int64_t* first_bad, int32_t accumulate, void* stream);
+
+/* Same as rb_point_pass on HOST buffers: pinned staging, chunked H2D copies
+ * overlapped with the point pass, results copied back to host; synchronous.
+ * The end-to-end entry a CPU caller of the reference would bind. */
+int rb_join_host(const rb_approx* a, const void* xy_host, int32_t xy_dtype, int64_t n, const float* attr_host,
+                 int64_t* cnt_host, double* sum_host, int64_t* first_bad_host);
+
+/* act.act_lookup: owner value per point (encoding above). */
+int rb_lookup(const rb_approx* a, const void* xy, int32_t xy_dtype, int64_t n, uint32_t* value_out,
+              int64_t* first_bad, void* stream);
+/* owner-list pool used by RB_VALUE_LIST values: *n = length; when dst is not
+ * NULL, copies the pool to dst (host or device memory, synchronous). */
+int rb_owner_pool(const rb_approx* a, uint32_t* dst, int64_t* n);
+
+/* grid.point_to_cell for a batch: leaf column/row. */
+int rb_point_cells(const rb_grid* grid, const void* xy, int32_t xy_dtype, int64_t n, uint32_t* ix, uint32_t* iy,
+                   int64_t* first_bad, void* stream);
+
+/* Covering export (RasterApprox) -- requires keep_cells.
+ * Two-call pattern: pass NULL arrays to get *n.  Device arrays, sorted by
+ * (polygon, level-L start code, level).  kind: 1 = interior, 2 = boundary. */
+int rb_approx_cells(const rb_approx* a, int64_t* n, int32_t* poly, int32_t* level, uint64_t* code, uint8_t* kind,
+                    void* stream);
+/* PARTIAL leaves (polygon, Z code, kept flag), sorted by (polygon, code). */
+int rb_approx_partial(const rb_approx* a, int64_t* n, int32_t* poly, uint64_t* code, uint8_t* kept, void* stream);
+
+/* geometry.point_in_polygon / distance_to_boundary on the
+ * GPU, for the epsilon validator: point k is tested against polygon
+ * poly_of_point[k] of `polys` (original coordinates). */
+int rb_exact_pip(const rb_polygons* polys, const double* px, const double* py, const int32_t* poly_of_point, int64_t n,
+                 uint8_t* inside_out, void* stream);
+int rb_exact_distance(const rb_polygons* polys, const double* px, const double* py, const int32_t* poly_of_point,
+                      int64_t n, double* dist_out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RASTERBOUND_B200_H */

@@ -1,0 +1,229 @@
+// rb_internal.cuh -- shared device helpers and the rb_approx handle.
+//
+// Geometry predicates here restate SPEC.md's semantics with the SAME float64
+// operation order as oracle/rb_oracle.c (the library is compiled with
+// --fmad=false so no multiply-add is contracted); that is what makes COUNT
+// parity bit-exact by construction.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/rasterbound_b200.h"
+
+#define RB_KIND_NONE 0
+#define RB_KIND_I 1
+#define RB_KIND_B 2
+
+// TRIE slot tag for "child node" (never returned by rb_lookup).
+#define RB_VALUE_NODE 0x80000000u
+
+namespace rb {
+
+void set_error(const std::string& msg);
+int fail(int status, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+
+#define RB_CUDA(call)                                   \
+  do {                                                  \
+    cudaError_t _e = (call);                            \
+    if (_e != cudaSuccess) return rb::cuda_fail(_e, #call); \
+  } while (0)
+
+// ------------------------------------------------------------------ grid
+struct GridD {
+  double ox, oy, side;
+  double lim;  // 2^L
+  int L;
+};
+
+__host__ __device__ inline uint64_t part1by1(uint64_t v) {
+  v &= 0xffffffffull;
+  v = (v | (v << 16)) & 0x0000ffff0000ffffull;
+  v = (v | (v << 8)) & 0x00ff00ff00ff00ffull;
+  v = (v | (v << 4)) & 0x0f0f0f0f0f0f0f0full;
+  v = (v | (v << 2)) & 0x3333333333333333ull;
+  v = (v | (v << 1)) & 0x5555555555555555ull;
+  return v;
+}
+__host__ __device__ inline uint64_t zenc(uint64_t ix, uint64_t iy) { return part1by1(ix) | (part1by1(iy) << 1); }
+__host__ __device__ inline uint32_t compact1by1(uint64_t v) {
+  v &= 0x5555555555555555ull;
+  v = (v | (v >> 1)) & 0x3333333333333333ull;
+  v = (v | (v >> 2)) & 0x0f0f0f0f0f0f0f0full;
+  v = (v | (v >> 4)) & 0x00ff00ff00ff00ffull;
+  v = (v | (v >> 8)) & 0x0000ffff0000ffffull;
+  v = (v | (v >> 16)) & 0x00000000ffffffffull;
+  return (uint32_t)v;
+}
+
+// S1: grid coordinate, correctly rounded division.
+__device__ __forceinline__ double gcoord(double v, double o, double side) { return __ddiv_rn(__dsub_rn(v, o), side); }
+
+// floor(RN((v - o) / side)) without a division on the common path: the
+// product with RN(1/side) is within 4e-16 relative of the quotient, so unless
+// it lies within 2^-20 of an integer its floor is the floor of the quotient;
+// otherwise fall back to the exact division (bit-identical to the oracle).
+__device__ __forceinline__ double cell_floor(double v, double o, double side, double inv_side) {
+  double d = __dsub_rn(v, o);
+  double q = __dmul_rn(d, inv_side);
+  double f = floor(q);
+  double fr = __dsub_rn(q, f);
+  if (fabs(__dsub_rn(fr, 0.5)) > 0.4999990463256836) f = floor(__ddiv_rn(d, side));
+  return f;
+}
+
+// S2 fixed formula (oracle y_at)
+__host__ __device__ inline double y_at(double x1, double y1, double x2, double y2, double c) {
+  if (c == x1) return y1;
+  if (c == x2) return y2;
+#ifdef __CUDA_ARCH__
+  double t = __dmul_rn(__dsub_rn(c, x1), __dsub_rn(y2, y1));
+  t = __ddiv_rn(t, __dsub_rn(x2, x1));
+  return __dadd_rn(y1, t);
+#else
+  double t = (c - x1) * (y2 - y1);
+  t = t / (x2 - x1);
+  return y1 + t;
+#endif
+}
+
+// scanline crossing abscissa (oracle x_cross), edge ordered yl < yh
+__host__ __device__ inline double x_cross(double xl, double yl, double xh, double yh, double yc) {
+#ifdef __CUDA_ARCH__
+  double t = __dmul_rn(__dsub_rn(yc, yl), __dsub_rn(xh, xl));
+  t = __ddiv_rn(t, __dsub_rn(yh, yl));
+  return __dadd_rn(xl, t);
+#else
+  double t = (yc - yl) * (xh - xl);
+  t = t / (yh - yl);
+  return xl + t;
+#endif
+}
+
+// SPEC.md:49-57 PIP, boundary = inside, even-odd over rings [r0, r1).
+__device__ inline int pip_rings(const double* X, const double* Y, const int64_t* ring_off, int64_t r0, int64_t r1,
+                                double px, double py) {
+  int inside = 0;
+  for (int64_t r = r0; r < r1; ++r) {
+    int64_t a = ring_off[r], b = ring_off[r + 1];
+    for (int64_t k = a; k < b; ++k) {
+      int64_t k2 = (k + 1 < b) ? k + 1 : a;
+      double ax = X[k], ay = Y[k], bx = X[k2], by = Y[k2];
+      double minx = ax < bx ? ax : bx, maxx = ax < bx ? bx : ax;
+      double miny = ay < by ? ay : by, maxy = ay < by ? by : ay;
+      if (px >= minx && px <= maxx && py >= miny && py <= maxy) {
+        double cr = __dsub_rn(__dmul_rn(__dsub_rn(bx, ax), __dsub_rn(py, ay)),
+                              __dmul_rn(__dsub_rn(by, ay), __dsub_rn(px, ax)));
+        if (cr == 0.0) return 1;
+      }
+      if ((ay > py) != (by > py)) {
+        double xl, yl, xh, yh;
+        if (ay < by) { xl = ax; yl = ay; xh = bx; yh = by; } else { xl = bx; yl = by; xh = ax; yh = ay; }
+        double xc = x_cross(xl, yl, xh, yh, py);
+        if (px == xc) return 1;
+        if (px < xc) inside = !inside;
+      }
+    }
+  }
+  return inside;
+}
+
+// SPEC.md:58-66 distance_to_boundary
+__device__ inline double dist_rings(const double* X, const double* Y, const int64_t* ring_off, int64_t r0, int64_t r1,
+                                    double px, double py) {
+  double best = INFINITY;
+  for (int64_t r = r0; r < r1; ++r) {
+    int64_t a = ring_off[r], b = ring_off[r + 1];
+    for (int64_t k = a; k < b; ++k) {
+      int64_t k2 = (k + 1 < b) ? k + 1 : a;
+      double ax = X[k], ay = Y[k], bx = X[k2], by = Y[k2];
+      double dx = bx - ax, dy = by - ay, wx = px - ax, wy = py - ay;
+      double L2 = dx * dx + dy * dy, t = 0.0;
+      if (L2 > 0.0) { t = (wx * dx + wy * dy) / L2; t = t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t); }
+      double ex = wx - t * dx, ey = wy - t * dy;
+      double d = sqrt(ex * ex + ey * ey);
+      best = d < best ? d : best;
+    }
+  }
+  return best;
+}
+
+// ----------------------------------------------------------- device buffer
+struct DBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
+  DBuf& operator=(DBuf&& o) noexcept { release(); p = o.p; bytes = o.bytes; o.p = nullptr; o.bytes = 0; return *this; }
+  ~DBuf() { release(); }
+  void release() { if (p) cudaFree(p); p = nullptr; bytes = 0; }
+  cudaError_t alloc(size_t b) { release(); bytes = b; return b ? cudaMalloc(&p, b) : cudaSuccess; }
+  template <class T> T* as() const { return (T*)p; }
+};
+
+// Index geometry: root table at level T0 (row-major, 2^T0 x 2^T0 slots) and
+// node levels T0 + ks[0], T0 + ks[0] + ks[1], ..., L; a node of level i holds
+// 2^ks[i] x 2^ks[i] row-major slots.  T0 == L is the dense uniform grid.
+#define RB_MAX_NODE_LEVELS 8
+struct IndexView {
+  const uint32_t* root;
+  const uint32_t* nodes[RB_MAX_NODE_LEVELS];
+  int ks[RB_MAX_NODE_LEVELS];
+  int nlev;
+  const uint32_t* pool;
+  int L, T0;
+};
+
+// Owner value of leaf (ix, iy): descend the radix table (ACT lookup,
+// every terminal on the path is collected; after the overlay
+// a slot holds either a child pointer or the complete owner value).
+__device__ __forceinline__ uint32_t index_lookup(const IndexView& v, uint32_t ix, uint32_t iy) {
+  int s = v.L - v.T0;
+  uint32_t val = __ldg(&v.root[((size_t)(iy >> s) << v.T0) | (ix >> s)]);
+#pragma unroll
+  for (int li = 0; li < RB_MAX_NODE_LEVELS; ++li) {
+    if (!(val & RB_VALUE_NODE)) break;
+    int k = v.ks[li];
+    s -= k;
+    uint32_t m = (1u << k) - 1u;
+    size_t node = val & RB_VALUE_PAYLOAD;
+    uint32_t slot = (((iy >> s) & m) << k) | ((ix >> s) & m);
+    val = __ldg(&v.nodes[li][(node << (2 * k)) + slot]);
+  }
+  return val;
+}
+
+}  // namespace rb
+
+struct rb_approx {
+  rb_grid grid;
+  rb_build_opts opts;
+  int32_t n_regions = 0;
+  int64_t n_polygons = 0;
+  rb::DBuf root, pool;
+  std::vector<rb::DBuf> node_bufs;
+  std::vector<int> node_levels;
+  int64_t root_entries = 0, n_nodes = 0, pool_len = 0;
+  int T0 = 0, k = 4;
+  // optional exports
+  rb::DBuf cell_poly, cell_level, cell_code, cell_kind;
+  int64_t n_cells = 0;
+  rb::DBuf part_poly, part_code, part_kept;
+  int64_t n_partial = 0;
+  rb_stats stats{};
+  rb::IndexView view() const {
+    rb::IndexView v{};
+    v.root = root.as<uint32_t>();
+    v.nlev = (int)node_levels.size();
+    for (int i = 0; i < v.nlev; ++i) { v.nodes[i] = node_bufs[i].as<uint32_t>(); v.ks[i] = node_levels[i]; }
+    v.pool = pool.as<uint32_t>();
+    v.L = grid.max_level;
+    v.T0 = T0;
+    return v;
+  }
+};

@@ -1,0 +1,227 @@
+"""Device-resident approximation + cell index (owner of an rb_approx handle).
+
+`ApproxIndex` is what raster / act / query share: it builds the epsilon-
+bounded raster approximation of a region set on the GPU (rb_approx_build),
+keeps the cell index resident in HBM and runs the point pass
+(rb_point_pass), the lookup (rb_lookup) and the host-buffer join
+(rb_join_host).  Immutable after construction; point passes on one index may
+run concurrently.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from . import errors as E
+from .geometry import DevicePolygons, PackedRegions
+from .grid import GridConfig
+
+INT64_MAX = (1 << 63) - 1
+LAYOUTS = {"dense": N.LAYOUT_DENSE, "trie": N.LAYOUT_TRIE}
+
+
+@dataclass
+class PassResult:
+    """Device tensors of one point pass: cnt [R,2] int64 (alpha, beta), sum [R,2] float64."""
+    cnt: object
+    sum: object
+    first_bad: object
+
+    def check(self):
+        b = int(self.first_bad.item())
+        if b != INT64_MAX:
+            raise E.DomainError(f"point {b} lies outside the grid domain or is NaN (SPEC.md:147)", b)
+        return self
+
+
+class ApproxIndex:
+    def __init__(self, packed: PackedRegions, grid: GridConfig, mode: int = N.MODE_CONSERVATIVE,
+                 layout: str = "trie", radix_width: int = 8, root_level: int = -1, keep_cells: bool = False,
+                 stream=None):
+        torch = N.require_cuda()
+        if layout not in LAYOUTS:
+            raise E.ConfigError(f"unknown layout {layout!r} (dense | trie)")
+        self.packed = packed
+        self.grid = grid
+        self.mode = int(mode)
+        self.layout = layout
+        self.radix_width = int(radix_width)
+        self.n_regions = packed.n_regions
+        self._dev = DevicePolygons(packed)
+        self._lib = N.load()
+        g = grid.native()
+        opts = N.BuildOpts(self.mode, LAYOUTS[layout], self.radix_width, int(root_level), 1 if keep_cells else 0)
+        h = C.c_void_p()
+        N.check(self._lib.rb_approx_build(C.byref(g), C.byref(self._dev.desc), C.byref(opts), N.stream_ptr(stream),
+                                          C.byref(h)), "rasterize/act_build")
+        self._h = h
+        self._torch = torch
+
+    @classmethod
+    def from_handle(cls, handle: C.c_void_p, grid: GridConfig, n_regions: int, layout: str, radix_width: int):
+        self = cls.__new__(cls)
+        self.packed = None
+        self.grid = grid
+        self.mode = -1
+        self.layout = layout
+        self.radix_width = radix_width
+        self.n_regions = n_regions
+        self._dev = None
+        self._lib = N.load()
+        self._h = handle
+        self._torch = N.require_cuda()
+        return self
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                self._torch.cuda.synchronize()
+            except Exception:
+                pass
+            self._lib.rb_approx_free(h)
+            self._h = None
+
+    @property
+    def handle(self) -> int:
+        return self._h.value
+
+    def stats(self) -> dict:
+        s = N.Stats()
+        N.check(self._lib.rb_approx_stats(self._h, C.byref(s)))
+        return s.as_dict()
+
+    # ------------------------------------------------------------ points
+    def _xy(self, xy):
+        torch = self._torch
+        t = xy if isinstance(xy, torch.Tensor) else torch.as_tensor(np.asarray(xy))
+        if t.dtype not in (torch.float64, torch.float32):
+            t = t.to(torch.float64)
+        if t.dim() != 2 or t.shape[1] != 2:
+            raise E.ShapeError("points must be an (N, 2) array")
+        t = t.to("cuda", non_blocking=True).contiguous()
+        return t, (N.XY_F64 if t.dtype == torch.float64 else N.XY_F32)
+
+    def point_pass(self, xy, attr=None, out: PassResult | None = None, accumulate: bool = False,
+                   stream=None) -> PassResult:
+        """Stream-ordered alpha/beta COUNT + SUM over device points (no host sync)."""
+        torch = self._torch
+        t, dt = self._xy(xy)
+        n = int(t.shape[0])
+        a = None
+        if attr is not None:
+            a = attr if isinstance(attr, torch.Tensor) else torch.as_tensor(np.asarray(attr))
+            a = a.to("cuda", dtype=torch.float32, non_blocking=True).contiguous()
+            if a.shape[0] != n:
+                raise E.ShapeError("attribute length differs from the point count")
+        if out is None:
+            out = PassResult(torch.empty((self.n_regions, 2), dtype=torch.int64, device="cuda"),
+                             torch.empty((self.n_regions, 2), dtype=torch.float64, device="cuda"),
+                             torch.empty(1, dtype=torch.int64, device="cuda"))
+        N.check(self._lib.rb_point_pass(self._h, t.data_ptr(), dt, n, a.data_ptr() if a is not None else None,
+                                        out.cnt.data_ptr(), out.sum.data_ptr(), out.first_bad.data_ptr(),
+                                        1 if accumulate else 0, N.stream_ptr(stream)), "join")
+        return out
+
+    def join_host(self, xy: np.ndarray, attr: np.ndarray | None = None):
+        """rb_join_host: host (ideally pinned) buffers in, host results out."""
+        xy = np.ascontiguousarray(xy) if isinstance(xy, np.ndarray) else xy
+        if isinstance(xy, np.ndarray):
+            dt = N.XY_F64 if xy.dtype == np.float64 else N.XY_F32
+            if xy.dtype not in (np.float64, np.float32):
+                raise E.ConfigError("xy must be float64 or float32")
+            ptr, n = xy.ctypes.data, xy.shape[0]
+        else:  # torch CPU (possibly pinned) tensor
+            dt = N.XY_F64 if xy.dtype == self._torch.float64 else N.XY_F32
+            ptr, n = xy.data_ptr(), int(xy.shape[0])
+        aptr = None
+        if attr is not None:
+            if isinstance(attr, np.ndarray):
+                attr = np.ascontiguousarray(attr, np.float32)
+                aptr = attr.ctypes.data
+            else:
+                aptr = attr.data_ptr()
+        cnt = np.zeros((self.n_regions, 2), np.int64)
+        sm = np.zeros((self.n_regions, 2), np.float64)
+        bad = np.zeros(1, np.int64)
+        N.check(self._lib.rb_join_host(self._h, ptr, dt, n, aptr, cnt.ctypes.data, sm.ctypes.data, bad.ctypes.data),
+                "join")
+        if int(bad[0]) != INT64_MAX:
+            raise E.DomainError(f"point {int(bad[0])} lies outside the grid domain or is NaN (SPEC.md:147)", int(bad[0]))
+        return cnt, sm
+
+    def lookup(self, xy, stream=None):
+        """Owner value per point (uint32 encoding of include/rasterbound_b200.h)."""
+        torch = self._torch
+        t, dt = self._xy(xy)
+        n = int(t.shape[0])
+        out = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+        bad = torch.empty(1, dtype=torch.int64, device="cuda")
+        N.check(self._lib.rb_lookup(self._h, t.data_ptr(), dt, n, out.data_ptr(), bad.data_ptr(), N.stream_ptr(stream)),
+                "act_lookup")
+        b = int(bad.item())
+        if b != INT64_MAX:
+            raise E.DomainError(f"point {b} lies outside the grid domain or is NaN (SPEC.md:147)", b)
+        return out[:n]
+
+    def owner_pool(self) -> np.ndarray:
+        n = C.c_int64()
+        N.check(self._lib.rb_owner_pool(self._h, None, C.byref(n)))
+        out = np.zeros(max(n.value, 1), np.uint32)
+        if n.value:
+            N.check(self._lib.rb_owner_pool(self._h, out.ctypes.data, C.byref(n)))
+        return out[: n.value]
+
+    def decode(self, values) -> list[list[tuple[int, int]]]:
+        """Owner values -> per point list of (dense region index, boundary flag)."""
+        vals = np.asarray(values.cpu().numpy() if hasattr(values, "cpu") else values).view(np.uint32)
+        pool = self.owner_pool()
+        out = []
+        for v in vals.tolist():
+            if v == 0:
+                out.append([])
+            elif not (v & N.VALUE_LIST):
+                s = v - 1
+                out.append([(s >> 1, s & 1)])
+            else:
+                off = v & N.VALUE_PAYLOAD
+                k = int(pool[off])
+                out.append([(int(e) >> 1, int(e) & 1) for e in pool[off + 1: off + 1 + k]])
+        return out
+
+    # ------------------------------------------------------------ exports
+    def cells(self):
+        """Per-polygon covering cells: (poly, level, code, kind) numpy arrays."""
+        torch = self._torch
+        n = C.c_int64()
+        N.check(self._lib.rb_approx_cells(self._h, C.byref(n), None, None, None, None, None))
+        m = n.value
+        poly = torch.empty(max(m, 1), dtype=torch.int32, device="cuda")
+        level = torch.empty(max(m, 1), dtype=torch.int32, device="cuda")
+        code = torch.empty(max(m, 1), dtype=torch.int64, device="cuda")
+        kind = torch.empty(max(m, 1), dtype=torch.uint8, device="cuda")
+        N.check(self._lib.rb_approx_cells(self._h, C.byref(n), poly.data_ptr(), level.data_ptr(), code.data_ptr(),
+                                          kind.data_ptr(), N.stream_ptr()))
+        torch.cuda.synchronize()
+        return (poly[:m].cpu().numpy(), level[:m].cpu().numpy(), code[:m].cpu().numpy().view(np.uint64),
+                kind[:m].cpu().numpy())
+
+    def partial(self):
+        """PARTIAL leaves: (poly, code, kept) numpy arrays sorted by (poly, code)."""
+        torch = self._torch
+        n = C.c_int64()
+        N.check(self._lib.rb_approx_partial(self._h, C.byref(n), None, None, None, None))
+        m = n.value
+        poly = torch.empty(max(m, 1), dtype=torch.int32, device="cuda")
+        code = torch.empty(max(m, 1), dtype=torch.int64, device="cuda")
+        kept = torch.empty(max(m, 1), dtype=torch.uint8, device="cuda")
+        N.check(self._lib.rb_approx_partial(self._h, C.byref(n), poly.data_ptr(), code.data_ptr(), kept.data_ptr(),
+                                            N.stream_ptr()))
+        torch.cuda.synchronize()
+        return poly[:m].cpu().numpy(), code[:m].cpu().numpy().view(np.uint64), kept[:m].cpu().numpy().astype(bool)
+
+
+__all__ = ["ApproxIndex", "PassResult", "INT64_MAX", "LAYOUTS"]
