@@ -1,0 +1,335 @@
+#!/usr/bin/env python
+"""bench.py -- points/s of the epsilon-bounded point-polygon COUNT/SUM join
+(BASELINE.json metric) on B200, plus the reference CPU path.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c4|c1] [--layout trie|dense]
+  python bench.py --impl reference ...        (CPU oracle port on the host cores)
+
+One step = one point pass over this rank's batch of synthetic points (inputs
+resident in HBM, approximation prebuilt and replicated on every GPU), plus
+the NCCL all-reduce of the per-region [R,2] int64 COUNT and float64 SUM when
+N > 1 (weak scaling: every rank owns its own batch, seed = 0 + rank).
+Rank 0 prints ONE JSON line.  See DESIGN.md "Measurement".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "points/s for eps-bounded point-polygon COUNT/SUM join"
+CONFIGS = {
+    "c1": dict(workload="C1 CPU-runnable ref: 1M uniform f64 points, 100 jittered-grid tiling polygons, eps=1e-3, "
+                        "uniform raster, COUNT", points=1_000_000, bpp=16, dtype="f64"),
+    "c2": dict(workload="C2 city-scale: 100M f64 points (50-Gaussian mixture + 10% uniform over 40x40 km), "
+                        "fare f32, 260 jittered-Voronoi tiling polygons (100-500 vertices), eps=4.9 m, "
+                        "uniform raster, COUNT + SUM(fare)", points=100_000_000, bpp=20, dtype="f64"),
+    "c4": dict(workload="C4 fine-polygon: 1B f32-offset points (same mixture over 100x100 km), fare f32, 40,000 "
+                        "jittered-Voronoi polygons (10-30 vertices), eps=1 m, hierarchical raster, COUNT + SUM(fare)",
+               points=1_000_000_000, bpp=12, dtype="f32->f64"),
+}
+REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+           0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+           0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--layout", default=None, choices=["trie", "dense"])
+    ap.add_argument("--points", type=int, default=None, help="override points per GPU")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def workload(cfg: str, n: int, rank: int):
+    from paper_2010_12548_b200 import workloads as W
+
+    if cfg == "c1":
+        return W.c1(n=n, seed=0)
+    if cfg == "c2":
+        return W.c2(n=n, seed=rank, regions=W.city_regions(0))
+    return W.c4(n=n, seed=0, rank=rank)
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler(threading.Thread):
+    """nvidia-smi's clocks line via NVML, polled every ~2 ms during the timed region."""
+
+    def __init__(self, dev: int):
+        super().__init__(daemon=True)
+        self.dev = dev
+        self.samples = []
+        self.stop_ev = threading.Event()
+        self.ok = True
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(dev)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as ex:  # pragma: no cover
+            self.ok = False
+            self.err = str(ex)
+
+    def run(self):
+        if not self.ok:
+            return
+        nv = self.nv
+        get_r = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        while not self.stop_ev.is_set():
+            try:
+                self.samples.append((nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM), int(get_r(self.h))))
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": getattr(self, "max_mhz", None), "reasons": [], "samples": 0,
+                    "note": getattr(self, "err", "no samples")}
+        mhz = sorted(s[0] for s in self.samples)
+        bits = 0
+        for s in self.samples:
+            bits |= s[1]
+        reasons = [v for k, v in REASONS.items() if bits & k and k != 0x1]
+        return {"sm_mhz": mhz[len(mhz) // 2], "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def cpu_baseline(w, grid, mode, attr, target_s: float):
+    """The oracle port (oracle/librb_oracle.so, pthreads) on a bounded prefix."""
+    from oracle import oracle as O
+    from paper_2010_12548_b200.geometry import pack_regions
+
+    O.build_lib()
+    p = pack_regions(w.regions)
+    A = O.Approx((grid.origin.x, grid.origin.y, grid.extent, grid.max_level), p.vx, p.vy, p.ring_off, p.poly_ring_off,
+                 p.poly_region, p.n_regions, mode)
+    cores = len(os.sched_getaffinity(0))
+    cal = min(w.n, 2_000_000)
+    t = time.perf_counter()
+    A.join(w.xy[:cal], None if attr is None else attr[:cal], nthreads=cores)
+    rate = cal / max(time.perf_counter() - t, 1e-6)
+    m = int(min(w.n, max(cal, rate * target_s)))
+    t = time.perf_counter()
+    cnt, sm = A.join(w.xy[:m], None if attr is None else attr[:m], nthreads=cores)
+    dt = time.perf_counter() - t
+    return dict(value=m / dt, unit="points/s", cores=cores, kind="port",
+                sample=f"first {m} of {w.n} points of the same workload, one oracle join over {cores} threads "
+                       f"({dt:.1f} s)"), (m, cnt, sm)
+
+
+def run_ours(a):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2010_12548_b200 import _native as N
+    from paper_2010_12548_b200.engine import PassResult
+    from paper_2010_12548_b200.query import AggregationQuery, PreparedJoin
+    from paper_2010_12548_b200.raster import RasterMode
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", init_method="env://", device_id=torch.device("cuda", local))
+    C = CONFIGS[a.config]
+    n = a.points or C["points"]
+    w = workload(a.config, n, rank)
+    layout = a.layout or ("dense" if a.config == "c1" else "trie")
+    agg = "COUNT" if a.config == "c1" else "SUM:fare"
+    q = AggregationQuery(agg, w.epsilon, RasterMode.CONSERVATIVE)
+    prep = PreparedJoin(w.regions, q, w.grid, layout=layout)
+    st = prep.stats()
+    grid = prep.grid
+    xy = torch.from_numpy(w.xy).cuda()
+    attr_np = w.attrs.get("fare") if agg != "COUNT" else None
+    attr = torch.from_numpy(attr_np).cuda() if attr_np is not None else None
+    R = prep.n_regions
+    out = PassResult(torch.empty((R, 2), dtype=torch.int64, device="cuda"),
+                     torch.empty((R, 2), dtype=torch.float64, device="cuda"),
+                     torch.empty(1, dtype=torch.int64, device="cuda"))
+    stream = torch.cuda.current_stream()
+
+    def step():
+        prep.index.point_pass(xy, attr, out=out)
+        if world > 1:
+            dist.all_reduce(out.cnt)
+            dist.all_reduce(out.sum)
+
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+    out.check()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    N.instrument(1)
+    sampler = ClockSampler(local)
+    sampler.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(a.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    sampler.stop_ev.set()
+    sampler.join()
+    launches, timed, kms = N.instrument(0)
+    N.instrument(2)
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    value = world * n * a.steps / (ms / 1e3)
+    peak, peak_src = peaks()
+    k_ms = kms / max(timed, 1)
+    achieved = n * C["bpp"] / (k_ms / 1e3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", f"ncu_{a.config}_{layout}.json")
+    if os.path.exists(prof):
+        with open(prof) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
+    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
+            "kernel": "k_point_pass", "kernel_ms": round(k_ms, 4),
+            "algorithmic_bytes_per_point": C["bpp"], "points_per_launch": n}
+    # ---- e2e: public API on pinned host buffers (rb_join_host), every step
+    e2e = None
+    if not a.no_e2e:
+        xy_pin = torch.from_numpy(w.xy).pin_memory()
+        at_pin = torch.from_numpy(attr_np).pin_memory() if attr_np is not None else None
+        prep.index.join_host(xy_pin, at_pin)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        k2 = a.steps
+        for _ in range(k2):
+            cnt_h, sum_h = prep.index.join_host(xy_pin, at_pin)
+            if world > 1:
+                ct = torch.from_numpy(cnt_h).cuda()
+                dist.all_reduce(ct)
+                cnt_h = ct.cpu().numpy()
+        el = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([el], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t.item())
+        e2e = {"value": world * n * k2 / el, "unit": "points/s", "h2d_bytes_per_step": int(n * C["bpp"]),
+               "d2h_bytes_per_step": int(R * 32 + 8), "api": "PreparedJoin.index.join_host -> rb_join_host",
+               "ms_per_step": round(el / k2 * 1e3, 3)}
+    # ---- CPU baseline + parity on the same sample (rank 0, N = 1)
+    cpu = None
+    parity = None
+    if rank == 0 and world == 1 and not a.no_cpu:
+        cpu, (m, cnt_o, sum_o) = cpu_baseline(w, grid, 0, attr_np, a.cpu_seconds)
+        r = prep.index.point_pass(xy[:m], attr[:m] if attr is not None else None).check()
+        cnt_g = r.cnt.cpu().numpy()
+        ok_c = bool(np.array_equal(cnt_g, cnt_o))
+        rel = float(np.max(np.abs(r.sum.cpu().numpy() - sum_o) / np.maximum(np.abs(sum_o), 1e-30))) if attr is not None else 0.0
+        parity = {"points": m, "count_bit_exact": ok_c, "sum_max_rel_err": rel}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 1), "unit": "points/s", "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": round(ms / a.steps, 4), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": C["dtype"], "data": "synthetic (seeded generators, DESIGN.md Workloads)",
+            "config": {"workload": C["workload"], "points_per_gpu": n, "polygons": len(w.regions),
+                       "epsilon": w.epsilon, "max_level": grid.max_level, "mode": "CONSERVATIVE",
+                       "index": layout, "root_level": st["root_level"], "index_bytes": st["index_bytes"],
+                       "build_ms": round(st["build_ms"], 1), "parallelism": f"dp{world} (points sharded, "
+                       "approximation replicated, NCCL all-reduce of [R,2] COUNT/SUM)",
+                       "l2": f"inputs {n * C['bpp'] / 1e9:.1f} GB per pass > 126 MB L2; no flush needed"},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": sampler.summary(), "parity_vs_oracle": parity,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_reference(a):
+    """The reference's CPU path = the oracle port (the reference ships no
+    implementation; oracle/rb_oracle.c restates SPEC.md), all host threads."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    from paper_2010_12548_b200.geometry import pack_regions
+    from paper_2010_12548_b200.grid import level_for_bound
+
+    C = CONFIGS[a.config]
+    n = a.points or C["points"]
+    w = workload(a.config, n, 0)
+    L = level_for_bound(w.grid, w.epsilon)
+    grid = w.grid.with_level(L)
+    attr = w.attrs.get("fare") if a.config != "c1" else None
+    p = pack_regions(w.regions)
+    O.build_lib()
+    A = O.Approx((grid.origin.x, grid.origin.y, grid.extent, L), p.vx, p.vy, p.ring_off, p.poly_ring_off,
+                 p.poly_region, p.n_regions, 0)
+    cores = len(os.sched_getaffinity(0))
+    cal = min(n, 1_000_000)
+    t = time.perf_counter()
+    A.join(w.xy[:cal], None if attr is None else attr[:cal], nthreads=cores)
+    rate = cal / max(time.perf_counter() - t, 1e-6)
+    budget = 150.0 / max(a.steps + a.warmup, 1)  # whole run ~2.5 min
+    m = int(min(n, max(cal, rate * budget)))
+    xs = w.xy[:m]
+    at = None if attr is None else attr[:m]
+    for _ in range(a.warmup):
+        A.join(xs, at, nthreads=cores)
+    t = time.perf_counter()
+    for _ in range(a.steps):
+        A.join(xs, at, nthreads=cores)
+    el = time.perf_counter() - t
+    value = m * a.steps / el
+    sample = f"each step: first {m} of the {n} points of the same workload, oracle join over {cores} threads"
+    line = {
+        "metric": METRIC, "value": round(value, 1), "unit": "points/s", "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": round(el / a.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": C["dtype"], "data": "synthetic", "impl": "reference",
+        "config": {"workload": C["workload"], "points_per_gpu": n, "polygons": len(w.regions), "epsilon": w.epsilon,
+                   "max_level": L, "mode": "CONSERVATIVE"},
+        "cpu_baseline": {"value": round(value, 1), "unit": "points/s", "cores": cores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": round(value, 1), "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)

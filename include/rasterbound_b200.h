@@ -169,6 +169,13 @@ int rb_exact_pip(const rb_polygons* polys, const double* px, const double* py, c
 int rb_exact_distance(const rb_polygons* polys, const double* px, const double* py, const int32_t* poly_of_point,
                       int64_t n, double* dist_out, void* stream);
 
+/* Instrumentation (benchmarks): op 1 = reset counters and enable CUDA-event
+ * timing of the point-pass main kernel, op 2 = reset and disable, op 0 = read
+ * (synchronises the recorded events): launches of this library's point-pass
+ * kernels since the reset, number of timed main-kernel launches and their
+ * summed device time in ms. */
+int rb_instrument(int32_t op, int64_t* launches, int64_t* timed_launches, double* timed_ms);
+
 #ifdef __cplusplus
 }
 #endif

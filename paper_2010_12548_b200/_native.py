@@ -28,7 +28,7 @@ VALUE_PAYLOAD = 0x3FFFFFFF
 EXPORTS = (
     "rb_version", "rb_last_error", "rb_level_for_bound", "rb_approx_build", "rb_approx_stats", "rb_approx_free",
     "rb_point_pass", "rb_join_host", "rb_lookup", "rb_owner_pool", "rb_point_cells", "rb_approx_cells",
-    "rb_approx_partial", "rb_exact_pip", "rb_exact_distance", "rb_index_from_cells",
+    "rb_approx_partial", "rb_exact_pip", "rb_exact_distance", "rb_index_from_cells", "rb_instrument",
 )
 
 
@@ -89,6 +89,7 @@ def load() -> C.CDLL:
     L.rb_approx_partial.argtypes = [p, C.POINTER(i64), p, p, p, p]
     L.rb_exact_pip.argtypes = [C.POINTER(Polygons), p, p, p, i64, p, p]
     L.rb_exact_distance.argtypes = [C.POINTER(Polygons), p, p, p, i64, p, p]
+    L.rb_instrument.argtypes = [i32, C.POINTER(i64), C.POINTER(i64), C.POINTER(d)]
     for name in EXPORTS:
         getattr(L, name)  # AttributeError if an export is missing
     _lib = L
@@ -121,3 +122,11 @@ def stream_ptr(stream=None) -> int:
 
     s = stream if stream is not None else torch.cuda.current_stream()
     return s.cuda_stream
+
+
+def instrument(op: int):
+    """op 1: reset + time the point-pass kernel; 2: reset, no timing; 0: read
+    -> (launches, timed_launches, timed_ms)."""
+    a, b, c = C.c_int64(), C.c_int64(), C.c_double()
+    check(load().rb_instrument(op, C.byref(a), C.byref(b), C.byref(c)), "rb_instrument")
+    return int(a.value), int(b.value), float(c.value)

@@ -31,6 +31,7 @@ int point_cells(const rb_grid* g, const void* xy, int32_t dtype, int64_t n, uint
                 int64_t* first_bad, cudaStream_t s);
 int exact_pip(const rb_polygons* P, const double* px, const double* py, const int32_t* pp, int64_t n, uint8_t* out,
               cudaStream_t s);
+int instrument(int op, int64_t* launches, int64_t* timed, double* ms);
 int exact_distance(const rb_polygons* P, const double* px, const double* py, const int32_t* pp, int64_t n,
                    double* out, cudaStream_t s);
 
@@ -255,4 +256,9 @@ done:
   if (ks) { cudaStreamSynchronize(ks); cudaStreamDestroy(ks); }
   if (cs) cudaStreamDestroy(cs);
   return rc;
+}
+
+extern "C" int rb_instrument(int32_t op, int64_t* launches, int64_t* timed_launches, double* timed_ms) {
+  if (op < 0 || op > 2) return fail(RB_CONFIG_ERROR, "rb_instrument op must be 0, 1 or 2");
+  return instrument(op, launches, timed_launches, timed_ms);
 }

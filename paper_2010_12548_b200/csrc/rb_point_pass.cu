@@ -13,11 +13,44 @@
 // kernel reduces the rows in CTA order -- deterministic, no global atomics.
 // Region sets too large for shared memory accumulate straight into global
 // memory with native REDG.ADD.64 / REDG.ADD.F64.
+#include <atomic>
 #include <climits>
+#include <mutex>
+#include <utility>
+#include <vector>
 
 #include "rb_internal.cuh"
 
 namespace rb {
+
+// ---- instrumentation (rb_instrument): launches of this library's kernels and
+// CUDA-event time of the point-pass main kernel (bench.py roofline).
+std::atomic<int64_t> g_launches{0};
+static std::atomic<bool> g_timing{false};
+static std::mutex g_ev_mu;
+static std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_events;
+
+int instrument(int op, int64_t* launches, int64_t* timed, double* ms) {
+  std::lock_guard<std::mutex> lk(g_ev_mu);
+  if (op == 0) {
+    double tot = 0.0;
+    for (auto& e : g_events) {
+      RB_CUDA(cudaEventSynchronize(e.second));
+      float t = 0.f;
+      RB_CUDA(cudaEventElapsedTime(&t, e.first, e.second));
+      tot += t;
+    }
+    if (launches) *launches = g_launches.load();
+    if (timed) *timed = (int64_t)g_events.size();
+    if (ms) *ms = tot;
+    return RB_OK;
+  }
+  for (auto& e : g_events) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
+  g_events.clear();
+  g_launches = 0;
+  g_timing = (op == 1);
+  return RB_OK;
+}
 
 __device__ __forceinline__ void ld256(const void* p, uint64_t& a, uint64_t& b, uint64_t& c, uint64_t& d) {
   asm("ld.global.nc.L1::no_allocate.L2::evict_first.v4.u64 {%0,%1,%2,%3}, [%4];"
@@ -248,6 +281,7 @@ int point_pass(const rb_approx* A, const void* xy, int32_t dtype, int64_t n, con
   if (flags) {
     k_init_out<<<std::max(1, (R2 + 255) / 256), 256, 0, s>>>(cnt_out, sum_out, R2, flags, a.first_bad);
     RB_CUDA(cudaGetLastError());
+    ++g_launches;
   }
   if (n == 0) return RB_OK;
   void* scratch = nullptr;
@@ -257,16 +291,29 @@ int point_pass(const rb_approx* A, const void* xy, int32_t dtype, int64_t n, con
     a.part_cnt = (uint32_t*)scratch;
     a.part_sum = (double*)((char*)scratch + (size_t)blocks * R2 * 4);
   }
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  if (g_timing) {
+    RB_CUDA(cudaEventCreate(&ev0));
+    RB_CUDA(cudaEventCreate(&ev1));
+    RB_CUDA(cudaEventRecord(ev0, s));
+  }
   cudaError_t e;
   if (dtype == RB_XY_F64)
     e = smem_hist ? launch_a<0, true>(a, vec, blocks, smem, s) : launch_a<0, false>(a, vec, blocks, smem, s);
   else
     e = smem_hist ? launch_a<1, true>(a, vec, blocks, smem, s) : launch_a<1, false>(a, vec, blocks, smem, s);
   if (e) return cuda_fail(e, "k_point_pass");
+  ++g_launches;
+  if (g_timing) {
+    RB_CUDA(cudaEventRecord(ev1, s));
+    std::lock_guard<std::mutex> lk(g_ev_mu);
+    g_events.emplace_back(ev0, ev1);
+  }
   if (smem_hist) {
     k_reduce_rows<<<std::max(1, (R2 + 255) / 256), 256, 0, s>>>(a.part_cnt, a.part_sum, blocks, R2, attr != nullptr,
                                                                 1, cnt_out, sum_out);
     RB_CUDA(cudaGetLastError());
+    ++g_launches;
     RB_CUDA(cudaFreeAsync(scratch, s));
   }
   return RB_OK;
