@@ -129,8 +129,12 @@ class Approx:
             raise OracleError(st.value)
 
     def __del__(self):
-        if getattr(self, "_h", None):
-            lib().orc_free(self._h)
+        h = getattr(self, "_h", None)
+        if h and _lib is not None:
+            try:
+                _lib.orc_free(h)
+            except Exception:
+                pass
             self._h = None
 
     @property

@@ -11,7 +11,7 @@ import os
 from . import errors as E
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "librasterbound_b200.so")
+LIB_PATH = os.environ.get("RASTERBOUND_B200_LIB") or os.path.join(_HERE, "lib", "librasterbound_b200.so")
 
 RB_OK = 0
 _STATUS = {

@@ -14,6 +14,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <chrono>
 #include <cmath>
 #include <memory>
@@ -632,6 +633,32 @@ __global__ void k_compact_anc(const uint64_t* anc, const int64_t* flag, const in
   GRID_STRIDE(k, n) if (flag[k]) out[pos[k]] = anc[k];
 }
 
+// ---- shared-memory summary: level-S cell -> its single owner value when the
+// whole cell has one (non-list, non-node) root value, else 0xffff
+__global__ void k_summary(const uint32_t* root, int T0, int S, uint16_t* out) {
+  const int d = T0 - S;
+  const int64_t ncell = (int64_t)1 << (2 * S);
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t sub = (int64_t)1 << (2 * d);
+  for (int64_t c = warp; c < ncell; c += nw) {
+    const uint64_t sx = (uint64_t)c & ((1ull << S) - 1), sy = (uint64_t)c >> S;
+    const uint32_t first = root[((sy << d) << T0) | (sx << d)];
+    bool same = !(first & (RB_VALUE_NODE | RB_VALUE_LIST)) && first < 0xffffu;
+    // warp-uniform trip count: every lane runs every iteration
+    for (int64_t e0 = 0; e0 < sub && __all_sync(0xffffffffu, same); e0 += 32) {
+      const int64_t e = e0 + lane;
+      if (e < sub) {
+        const uint64_t rx = (sx << d) | ((uint64_t)e & ((1ull << d) - 1)), ry = (sy << d) | ((uint64_t)e >> d);
+        if (root[(ry << T0) | rx] != first) same = false;
+      }
+    }
+    same = __all_sync(0xffffffffu, same);
+    if (lane == 0) out[c] = same ? (uint16_t)first : (uint16_t)0xffffu;
+  }
+}
+
 // ---------------------------------------------------------------- driver
 struct Ctx {
   cudaStream_t s;
@@ -877,6 +904,19 @@ static int index_impl(int L, int64_t total_cells, const int32_t* cp_in, const ui
   }
   A->n_nodes = total_nodes;
   A->stats.n_nodes = total_nodes;
+  // summary table for the shared-memory fast path (owner values must fit u16)
+  {
+    int Smax = 7;
+    if (const char* e = getenv("RB_SUMMARY_LEVEL")) Smax = atoi(e);
+    A->S = -1;
+    if (Smax >= 0 && 2 * (int64_t)A->n_regions + 1 < 0xffff) {
+      const int S = std::min(Smax, T0);
+      RB_CUDA(A->summary.alloc(((size_t)2 << (2 * S))));
+      k_summary<<<nblk(((int64_t)32 << (2 * S))), 256, 0, s>>>(A->root.as<uint32_t>(), T0, S, A->summary.as<uint16_t>());
+      RB_CUDA(cudaGetLastError());
+      A->S = S;
+    }
+  }
   A->stats.root_level = T0;
   A->stats.node_levels = k;
   A->stats.index_bytes = A->root_entries * 4 + node_bytes + npool * 4;

@@ -177,6 +177,8 @@ struct IndexView {
   int nlev;
   const uint32_t* pool;
   int L, T0;
+  const uint16_t* summary;  // level-S table of single owner values (0xffff = consult the index)
+  int S;
 };
 
 // Owner value of leaf (ix, iy): descend the radix table (ACT lookup,
@@ -210,6 +212,8 @@ struct rb_approx {
   std::vector<int> node_levels;
   int64_t root_entries = 0, n_nodes = 0, pool_len = 0;
   int T0 = 0, k = 4;
+  rb::DBuf summary;  // u16 [4^S] or empty
+  int S = -1;
   // optional exports
   rb::DBuf cell_poly, cell_level, cell_code, cell_kind;
   int64_t n_cells = 0;
@@ -224,6 +228,8 @@ struct rb_approx {
     v.pool = pool.as<uint32_t>();
     v.L = grid.max_level;
     v.T0 = T0;
+    v.summary = summary.as<uint16_t>();
+    v.S = S;
     return v;
   }
 };

@@ -14,6 +14,7 @@
 // Region sets too large for shared memory accumulate straight into global
 // memory with native REDG.ADD.64 / REDG.ADD.F64.
 #include <atomic>
+#include <cstdlib>
 #include <climits>
 #include <mutex>
 #include <utility>
@@ -79,6 +80,8 @@ struct PassArgs {
   double* gsum;
   unsigned long long* first_bad;
   int64_t idx_base;  // global index of point 0 (chunked host joins)
+  long long* part_acc;
+  const int* scale_exp;
 };
 
 template <bool SMEM, bool ATTR>
@@ -126,10 +129,11 @@ __device__ __forceinline__ void point(const PassArgs& a, Hist<SMEM, ATTR>& h, do
   }
 }
 
-// XY: 0 = f64 interleaved, 1 = f32 interleaved.  VEC: vectorised main loop.
+// Large region sets (histogram does not fit in shared memory): accumulate
+// straight into global memory.  XY: 0 = f64, 1 = f32.  VEC: 32-byte loads.
 template <int XY, bool SMEM, bool ATTR, bool VEC>
-__global__ void __launch_bounds__(512) k_point_pass(PassArgs a) {
-  extern __shared__ __align__(16) unsigned char smem[];
+__global__ void __launch_bounds__(512) k_point_pass_global(PassArgs a) {
+  extern __shared__ __align__(128) unsigned char smem[];
   Hist<SMEM, ATTR> h;
   h.a = &a;
   h.ssum = (double*)smem;
@@ -202,18 +206,706 @@ __global__ void __launch_bounds__(512) k_point_pass(PassArgs a) {
   }
 }
 
-// deterministic reduction of the per-CTA rows (fixed CTA order)
-__global__ void k_reduce_rows(const uint32_t* part_cnt, const double* part_sum, int nrows, int R2, bool attr,
-                              int accumulate, int64_t* cnt_out, double* sum_out) {
+
+// ---------------------------------------------------------------------------
+// Shared-memory histogram kernel (region sets up to RB_SMEM_MAX_REGIONS).
+//
+// * grid = SMs x resident CTAs (occupancy API); CTA b streams a contiguous
+//   range of 32-byte chunks, lane-interleaved so every load instruction of a
+//   warp covers 1 KB of consecutive memory;
+// * each thread handles PB = 8 points per iteration: all coordinates are
+//   loaded first, all leaf cells computed, then all root-table reads issued
+//   together, then each node level -- the dependent index chain overlaps
+//   across the 8 points instead of serialising per point;
+// * COUNT: native u32 smem atomics.  SUM: per-launch binary scale 2^S chosen
+//   from a sample of the attribute (k_attr_scale); values whose scaled
+//   magnitude lies in [2^20, 2^30) are accumulated exactly as int32 fixed
+//   point split over two u32 atomics (low 16 / signed high 16 bits), folded
+//   into int64 every 65536 points of the CTA; everything else (huge, tiny,
+//   non-finite) goes to a float64 slow path.  Relative quantisation error per
+//   value <= 2^-21 (< 1e-6), and the fixed-point part is order-independent.
+// ---------------------------------------------------------------------------
+#define RB_PB 8
+#ifndef RB_MINB
+#define RB_MINB 2
+#endif
+
+struct LevelDesc {
+  const uint32_t* nodes[RB_MAX_NODE_LEVELS];
+  int ks[RB_MAX_NODE_LEVELS];
+};
+
+template <bool ATTR>
+struct SHist {
+  uint32_t* cnt;
+  uint32_t* lo;
+  uint32_t* hi;
+  double* slow;
+  __device__ __forceinline__ void add_fast(uint32_t q, int32_t qv) {
+    atomicAdd(&cnt[q], 1u);
+    if (ATTR) {
+      atomicAdd(&lo[q], (uint32_t)qv & 0xffffu);
+      atomicAdd(&hi[q], (uint32_t)(qv >> 16));
+    }
+  }
+  __device__ __forceinline__ void add_slow(uint32_t q, float w) {
+    atomicAdd(&cnt[q], 1u);
+    if (ATTR) atomicAdd(&slow[q], (double)w);
+  }
+  __device__ __forceinline__ void add(uint32_t q, float w, int32_t qv, bool fast) {
+    if (fast) add_fast(q, qv); else add_slow(q, w);
+  }
+};
+
+// Interleaved shared-memory histogram for the TMA kernel: bin q owns words
+// h3[3q] (count), h3[3q+1] (fixed-point low 16 bits), h3[3q+2] (signed high
+// part); stride 3 is coprime with the 32 banks, one base IMAD per update.
+template <bool ATTR>
+struct IHist {
+  uint32_t* h3;
+  double* slow;
+  __device__ __forceinline__ void add_fast(uint32_t q, int32_t qv) {
+    uint32_t* b = h3 + (ATTR ? 3u * q : q);
+    atomicAdd(b, 1u);
+    if (ATTR) {
+      atomicAdd(b + 1, (uint32_t)qv & 0xffffu);
+      atomicAdd(b + 2, (uint32_t)(qv >> 16));
+    }
+  }
+  __device__ __forceinline__ void add_slow(uint32_t q, float w) {
+    atomicAdd(h3 + (ATTR ? 3u * q : q), 1u);
+    if (ATTR) atomicAdd(&slow[q], (double)w);
+  }
+  __device__ __forceinline__ void add(uint32_t q, float w, int32_t qv, bool fast) {
+    if (fast) add_fast(q, qv); else add_slow(q, w);
+  }
+};
+
+#ifndef RB_OWNERS_INLINE
+#define RB_OWNERS_ATTR __noinline__
+#else
+#define RB_OWNERS_ATTR __forceinline__
+#endif
+template <bool ATTR>
+__device__ RB_OWNERS_ATTR void add_owners_i(IHist<ATTR> h, const uint32_t* __restrict__ pool, uint32_t v, float w,
+                                          int32_t qv, bool fast) {
+  if (!(v & RB_VALUE_LIST)) {
+    const uint32_t sv = v - 1u, q = sv & ~1u;
+    h.add(q, w, qv, fast);
+    if (sv & 1u) h.add(q + 1, w, qv, fast);
+    return;
+  }
+  const uint32_t* Lp = pool + (v & RB_VALUE_PAYLOAD);
+  const uint32_t kk = __ldg(Lp);
+  for (uint32_t e = 1; e <= kk; ++e) {
+    const uint32_t ent = __ldg(Lp + e);
+    const uint32_t q = ent & ~1u;
+    h.add(q, w, qv, fast);
+    if (ent & 1u) h.add(q + 1, w, qv, fast);
+  }
+}
+
+// predicated 32-bit read-only load: returns dflt without touching memory when !pred
+__device__ __forceinline__ uint32_t ldg_pred(const uint32_t* ptr, bool pred, uint32_t dflt) {
+  uint32_t v;
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n mov.u32 %0, %3;\n @p ld.global.nc.u32 %0, [%1];\n}\n"
+      : "=r"(v)
+      : "l"(ptr), "r"((uint32_t)pred), "r"(dflt));
+  return v;
+}
+
+struct PassConst {
+  double ox, oy, side, inv_side, lim;
+  const uint32_t* root;
+  const uint32_t* pool;
+  uint32_t hmax;   // (2^L - 1) >> 12: bound on t's high word minus 0x41F00000
+  uint32_t lim_u;  // 2^L (exclusive, for L < 12)
+  int L, T0, s0, nlev;
+};
+
+// Rare path 1: exact division + domain check for a point
+// whose fast quantisation was not conclusive.  Returns false if out of domain.
+__device__ __noinline__ uint64_t quantize_exact(const void* xy, int64_t pidx, int XY, double ox, double oy, double side,
+                                                double lim, unsigned long long* first_bad, int64_t idx_base) {
+  double xx, yy;
+  if (XY == 0) { xx = ((const double*)xy)[2 * pidx]; yy = ((const double*)xy)[2 * pidx + 1]; }
+  else { xx = (double)((const float*)xy)[2 * pidx]; yy = (double)((const float*)xy)[2 * pidx + 1]; }
+  const double fx = floor(__ddiv_rn(__dsub_rn(xx, ox), side));
+  const double fy = floor(__ddiv_rn(__dsub_rn(yy, oy), side));
+  if (!(fx >= 0.0 && fx < lim && fy >= 0.0 && fy < lim)) {
+    atomicMin(first_bad, (unsigned long long)(idx_base + pidx));
+    return ~0ull;
+  }
+  return ((uint64_t)(uint32_t)fy << 32) | (uint32_t)fx;
+}
+
+// Rare path 2: owner lists and boundary owners (multi-owner cells).
+template <bool ATTR>
+__device__ __noinline__ void add_owners(SHist<ATTR> h, const uint32_t* __restrict__ pool, uint32_t v, float w,
+                                        int32_t qv, bool fast) {
+  if (!(v & RB_VALUE_LIST)) {
+    const uint32_t sv = v - 1u, q = sv & ~1u;
+    h.add(q, w, qv, fast);
+    h.add(q + 1, w, qv, fast);
+    return;
+  }
+  const uint32_t* Lp = pool + (v & RB_VALUE_PAYLOAD);
+  const uint32_t kk = __ldg(Lp);
+  for (uint32_t e = 1; e <= kk; ++e) {
+    const uint32_t ent = __ldg(Lp + e);
+    const uint32_t q = ent & ~1u;
+    h.add(q, w, qv, fast);
+    if (ent & 1u) h.add(q + 1, w, qv, fast);
+  }
+}
+
+template <int XY, bool ATTR, bool VEC>
+__global__ void __launch_bounds__(256, RB_MINB) k_point_pass(PassArgs a) {
+  constexpr int PPC = XY == 0 ? 2 : 4;  // points per 32-byte chunk
+  constexpr int CPT = RB_PB / PPC;      // chunks per thread per iteration
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ LevelDesc lv;
+  const int R2 = a.R2;
+  long long* acc = (long long*)smem;
+  double* slow = (double*)(smem + (size_t)R2 * 8);
+  uint32_t* cnt = (uint32_t*)(smem + (size_t)R2 * (ATTR ? 16 : 0));
+  SHist<ATTR> h{cnt, cnt + R2, cnt + 2 * R2, slow};
+  for (int q = threadIdx.x; q < R2; q += blockDim.x) {
+    cnt[q] = 0;
+    if (ATTR) { h.lo[q] = 0; h.hi[q] = 0; acc[q] = 0; slow[q] = 0.0; }
+  }
+  if (threadIdx.x < RB_MAX_NODE_LEVELS) {
+    lv.nodes[threadIdx.x] = a.V.nodes[threadIdx.x];
+    lv.ks[threadIdx.x] = a.V.ks[threadIdx.x];
+  }
+  __syncthreads();
+  float sc = 1.f, wmax = 0.f, wmin = 0.f;
+  if (ATTR) {
+    const int S = *a.scale_exp;
+    sc = __int_as_float((S + 127) << 23);
+    wmax = __int_as_float((30 - S + 127) << 23);
+    wmin = __int_as_float((20 - S + 127) << 23);
+  }
+  PassConst c;
+  c.ox = a.ox; c.oy = a.oy; c.side = a.side; c.inv_side = a.inv_side; c.lim = a.lim;
+  c.root = a.V.root; c.pool = a.V.pool;
+  c.L = a.V.L; c.T0 = a.V.T0; c.s0 = c.L - c.T0; c.nlev = a.V.nlev;
+  c.lim_u = c.L >= 32 ? 0xffffffffu : (1u << c.L);
+  c.hmax = (uint32_t)(((1ull << c.L) - 1ull) >> 12);
+  const int64_t nchunks = a.n / PPC;
+  const int64_t per_cta = (nchunks + gridDim.x - 1) / gridDim.x;
+  const int64_t c_beg = (int64_t)blockIdx.x * per_cta;
+  const int64_t c_end = c_beg + per_cta < nchunks ? c_beg + per_cta : nchunks;
+  const int64_t span = (int64_t)blockDim.x * CPT;
+  const int64_t iters = c_end > c_beg ? (c_end - c_beg + span - 1) / span : 0;
+  const int64_t epi = (65536 / (blockDim.x * RB_PB)) > 0 ? (65536 / (blockDim.x * RB_PB)) : 1;
+  const char* base = (const char*)a.xy;
+
+  for (int64_t it0 = 0; it0 < iters; it0 += epi) {
+    const int64_t it1 = it0 + epi < iters ? it0 + epi : iters;
+    for (int64_t it = it0; it < it1; ++it) {
+      uint32_t ix[RB_PB], iy[RB_PB], val[RB_PB];
+      float w[RB_PB];
+      uint32_t okm = 0, slowm = 0;
+      const int64_t cb = c_beg + it * span + threadIdx.x;
+      // 1. loads + quantisation.  t = RN(RN(RN(v - o) * inv_side) + 2^32)
+      //    holds floor(q) in mantissa bits 20..51 and q's fraction rounded to
+      //    2^-20 in bits 0..19; its high word minus 0x41F00000 is <= hmax iff
+      //    0 <= q < 2^32 and floor(q) >> 12 < 2^(L-12).  A point whose fraction
+      //    lies within 2^-19 of an integer, or that fails the range test, takes
+      //    the exact path (bit-identical to floor(RN(d / side))).
+#pragma unroll
+      for (int k = 0; k < CPT; ++k) {
+        const int64_t ch = cb + (int64_t)k * blockDim.x;
+        const bool v = ch < c_end;
+        uint64_t u[4] = {0, 0, 0, 0};
+        if (v) {
+          if (VEC) ld256(base + ch * 32, u[0], u[1], u[2], u[3]);
+          else {
+            const uint64_t* p = (const uint64_t*)(base + ch * 32);
+            u[0] = p[0]; u[1] = p[1]; u[2] = p[2]; u[3] = p[3];
+          }
+        }
+        if (ATTR) {
+          if (XY == 0) {
+            if (v) {
+              if (VEC) ld64f2(a.attr + 2 * ch, w[2 * k], w[2 * k + 1]);
+              else { w[2 * k] = a.attr[2 * ch]; w[2 * k + 1] = a.attr[2 * ch + 1]; }
+            } else { w[2 * k] = 0.f; w[2 * k + 1] = 0.f; }
+          } else {
+            if (v) {
+              if (VEC) ld128f4(a.attr + 4 * ch, w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
+              else {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) w[4 * k + j] = a.attr[4 * ch + j];
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 4; ++j) w[4 * k + j] = 0.f;
+            }
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < PPC; ++j) {
+          const int i = k * PPC + j;
+          double x, y;
+          if (XY == 0) { x = __longlong_as_double(u[2 * j]); y = __longlong_as_double(u[2 * j + 1]); }
+          else {
+            x = (double)__uint_as_float((uint32_t)u[j]);
+            y = (double)__uint_as_float((uint32_t)(u[j] >> 32));
+          }
+          const double tx = __dadd_rn(__dmul_rn(__dsub_rn(x, c.ox), c.inv_side), 4294967296.0);
+          const double ty = __dadd_rn(__dmul_rn(__dsub_rn(y, c.oy), c.inv_side), 4294967296.0);
+          const uint32_t lx = (uint32_t)__double2loint(tx), hx = (uint32_t)__double2hiint(tx);
+          const uint32_t ly = (uint32_t)__double2loint(ty), hy = (uint32_t)__double2hiint(ty);
+          ix[i] = __funnelshift_r(lx, hx, 20);
+          iy[i] = __funnelshift_r(ly, hy, 20);
+          const bool good = ((hx - 0x41F00000u) <= c.hmax) & ((hy - 0x41F00000u) <= c.hmax) &
+                            (((lx + 2u) & 0xfffffu) >= 4u) & (((ly + 2u) & 0xfffffu) >= 4u) &
+                            (ix[i] < c.lim_u) & (iy[i] < c.lim_u);
+          okm |= (v & good) ? (1u << i) : 0u;
+          slowm |= (v & !good) ? (1u << i) : 0u;
+        }
+      }
+      if (slowm) {
+#pragma unroll 1
+        for (uint32_t m = slowm; m; m &= m - 1) {
+          const int i = __ffs(m) - 1;
+          const int64_t pidx = (cb + (int64_t)(i / PPC) * blockDim.x) * PPC + (i % PPC);
+          const uint64_t qq = quantize_exact(a.xy, pidx, XY, c.ox, c.oy, c.side, c.lim, a.first_bad, a.idx_base);
+          const uint32_t qx = (uint32_t)qq, qy = (uint32_t)(qq >> 32);
+          if (qq != ~0ull) {
+            // write back through a switch so the arrays stay in registers
+#pragma unroll
+            for (int t = 0; t < RB_PB; ++t)
+              if (t == i) { ix[t] = qx; iy[t] = qy; }
+            okm |= 1u << i;
+          }
+        }
+      }
+      // 2. root reads for all points, then node levels (ACT descent)
+#pragma unroll
+      for (int i = 0; i < RB_PB; ++i) {
+        const uint32_t ri = ((iy[i] >> c.s0) << c.T0) | (ix[i] >> c.s0);
+        val[i] = (okm >> i) & 1u ? __ldg(c.root + ri) : 0u;
+      }
+      uint32_t nodem = 0;
+#pragma unroll
+      for (int i = 0; i < RB_PB; ++i) nodem |= (val[i] >> 31) << i;
+      if (nodem) {
+        int s = c.s0;
+#pragma unroll 1
+        for (int li = 0; li < c.nlev; ++li) {
+          const int k = lv.ks[li];
+          const uint32_t* __restrict__ nodes = lv.nodes[li];
+          s -= k;
+          const uint32_t m = (1u << k) - 1u;
+#pragma unroll
+          for (int i = 0; i < RB_PB; ++i) {
+            if (val[i] & RB_VALUE_NODE) {
+              const uint32_t slot = (((iy[i] >> s) & m) << k) | ((ix[i] >> s) & m);
+              val[i] = __ldg(nodes + (((val[i] & RB_VALUE_PAYLOAD) << (2 * k)) + slot));
+            }
+          }
+        }
+      }
+      // 3. accumulate: single interior owner inline, every
+      //    other owner value (boundary owner, owner list) on the outlined path
+#pragma unroll
+      for (int i = 0; i < RB_PB; ++i) {
+        const uint32_t v = val[i];
+        int32_t qv = 0;
+        bool fast = true;
+        if (ATTR) {
+          const float aw = fabsf(w[i]);
+          fast = (aw < wmax) & ((aw >= wmin) | (aw == 0.f));
+          qv = __float2int_rn(w[i] * sc);
+        }
+        const uint32_t sv = v - 1u;
+        if (v != 0u && (sv & (RB_VALUE_LIST | 1u)) == 0u) {
+          if (fast) h.add_fast(sv, qv); else h.add_slow(sv, w[i]);
+        } else if (v != 0u) {
+          add_owners<ATTR>(h, c.pool, v, w[i], qv, fast);
+        }
+      }
+    }
+    if (ATTR) {
+      __syncthreads();
+      for (int q = threadIdx.x; q < R2; q += blockDim.x) {
+        acc[q] += ((long long)(int32_t)h.hi[q] << 16) + (long long)h.lo[q];
+        h.lo[q] = 0;
+        h.hi[q] = 0;
+      }
+      __syncthreads();
+    }
+  }
+  // remainder points (n not a multiple of the chunk): last CTA, float64 path
+  if (blockIdx.x == gridDim.x - 1) {
+    for (int64_t i = nchunks * PPC + threadIdx.x; i < a.n; i += blockDim.x) {
+      const uint64_t qq = quantize_exact(a.xy, i, XY, c.ox, c.oy, c.side, c.lim, a.first_bad, a.idx_base);
+      if (qq == ~0ull) continue;
+      const uint32_t qx = (uint32_t)qq, qy = (uint32_t)(qq >> 32);
+      const uint32_t v = index_lookup(a.V, qx, qy);
+      if (v == 0) continue;
+      const float ww = ATTR ? a.attr[i] : 0.f;
+      if (!(v & RB_VALUE_LIST) && !((v - 1u) & 1u)) h.add_slow(v - 1u, ww);
+      else add_owners<ATTR>(h, c.pool, v, ww, 0, false);
+    }
+  }
+  __syncthreads();
+  uint32_t* pc = a.part_cnt + (size_t)blockIdx.x * R2;
+  long long* pa = a.part_acc + (size_t)blockIdx.x * R2;
+  double* ps = a.part_sum + (size_t)blockIdx.x * R2;
+  for (int q = threadIdx.x; q < R2; q += blockDim.x) {
+    pc[q] = cnt[q];
+    if (ATTR) { pa[q] = acc[q]; ps[q] = slow[q]; }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// TMA-staged point pass (the production path).
+//
+// Warp 0 is the producer: one elected lane streams fixed-size tiles of the
+// coordinate and attribute columns into a 4-stage shared-memory ring with
+// cp.async.bulk (1-D TMA, L2 evict-first policy, completion on an mbarrier).
+// Warps 1..8 consume: each thread takes 4 points of the tile from shared
+// memory, quantises them, walks the radix table and accumulates.  DRAM
+// latency is absorbed by the ring; no registers are tied up by in-flight
+// loads, so the consumers only wait on the L2-resident index.
+// ---------------------------------------------------------------------------
+#ifndef RB_TP
+#define RB_TP 1024     // points per tile
+#endif
+#ifndef RB_NST
+#define RB_NST 3       // ring stages
+#endif
+#ifndef RB_LATE_RELEASE
+#define RB_LATE_RELEASE 0
+#endif
+#ifndef RB_DEBUG_CHECK
+#define RB_DEBUG_CHECK 0
+#endif
+#ifndef RB_DEBUG_SLOWSUM
+#define RB_DEBUG_SLOWSUM 0
+#endif
+#ifndef RB_EXPERIMENT
+#define RB_EXPERIMENT 0  // ablations for profiling: 1 no histogram, 2 no index, 3 both ... see tools/
+#endif
+#define RB_CONS 256    // consumer threads
+#define RB_PPT (RB_TP / RB_CONS)
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+          smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+
+template <int XY, bool ATTR>
+__global__ void __launch_bounds__(RB_CONS + 32, 2) k_point_pass_tma(PassArgs a) {
+  constexpr int PB_BYTES = XY == 0 ? 16 : 8;
+  constexpr uint32_t XY_TILE = RB_TP * PB_BYTES;
+  constexpr uint32_t AT_TILE = ATTR ? RB_TP * 4 : 0;
+  constexpr uint32_t STAGE = XY_TILE + AT_TILE;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ LevelDesc lv;
+  __shared__ __align__(8) uint64_t full_bar[RB_NST], empty_bar[RB_NST];
+  const int R2 = a.R2;
+  // layout: [ring][h3: R2*(ATTR?3:1) u32][acc: R2 i64][slow: R2 f64][summary u16]
+  unsigned char* hist = smem + (size_t)RB_NST * STAGE;
+  uint32_t* h3 = (uint32_t*)hist;
+  const size_t h3_bytes = (((size_t)R2 * (ATTR ? 12 : 4)) + 15) & ~(size_t)15;
+  long long* acc = (long long*)(hist + h3_bytes);
+  double* slow = (double*)(hist + h3_bytes + (ATTR ? (size_t)R2 * 8 : 0));
+  uint16_t* summ = (uint16_t*)(hist + h3_bytes + (ATTR ? (size_t)R2 * 16 : 0));
+  IHist<ATTR> h{h3, slow};
+  const int tid = threadIdx.x;
+  const int S = a.V.S;
+  for (int q = tid; q < R2 * (ATTR ? 3 : 1); q += blockDim.x) h3[q] = 0;
+  if (ATTR)
+    for (int q = tid; q < R2; q += blockDim.x) { acc[q] = 0; slow[q] = 0.0; }
+  if (S >= 0) {
+    const int nsum = 1 << (2 * S);
+    const uint4* src = (const uint4*)a.V.summary;
+    uint4* dst = (uint4*)summ;
+    for (int q = tid; q < (nsum >> 3); q += blockDim.x) dst[q] = __ldg(src + q);
+    for (int q = (nsum & ~7) + tid; q < nsum; q += blockDim.x) summ[q] = a.V.summary[q];
+  }
+  if (tid < RB_MAX_NODE_LEVELS) {
+    lv.nodes[tid] = a.V.nodes[tid];
+    lv.ks[tid] = a.V.ks[tid];
+  }
+  if (tid == 0) {
+    for (int s = 0; s < RB_NST; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], RB_CONS / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t nmain = a.n & ~(int64_t)3;  // bulk copies need 16-byte granules
+  const int64_t ntiles = (nmain + RB_TP - 1) / RB_TP;
+  const int64_t G = gridDim.x;
+
+  if (tid < 32) {
+    // ------------------------------------------------------------ producer
+    if (tid == 0) {
+      uint64_t pol;
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+      int st = 0;
+      uint32_t ph = 0;
+      int64_t k = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += G, ++k) {
+        if (k >= RB_NST) mbar_wait(&empty_bar[st], ph ^ 1u);
+        const int64_t p0 = t * RB_TP;
+        const uint32_t m = (uint32_t)(p0 + RB_TP <= nmain ? RB_TP : nmain - p0);
+        unsigned char* dst = smem + (size_t)st * STAGE;
+        mbar_expect_tx(&full_bar[st], m * PB_BYTES + (ATTR ? m * 4 : 0));
+        bulk_g2s(dst, (const char*)a.xy + p0 * PB_BYTES, m * PB_BYTES, &full_bar[st], pol);
+        if (ATTR) bulk_g2s(dst + XY_TILE, a.attr + p0, m * 4, &full_bar[st], pol);
+        if (++st == RB_NST) { st = 0; ph ^= 1u; }
+      }
+    }
+    return;
+  }
+  // -------------------------------------------------------------- consumers
+  const int ct = tid - 32;
+  float sc = 1.f, wmax = 0.f, wmin = 0.f;
+  if (ATTR) {
+    const int Sx = *a.scale_exp;
+    sc = __int_as_float((Sx + 127) << 23);
+    wmax = __int_as_float((30 - Sx + 127) << 23);
+    wmin = __int_as_float((20 - Sx + 127) << 23);
+  }
+  const double ox = a.ox, oy = a.oy, inv_side = a.inv_side;
+  const uint32_t* __restrict__ root = a.V.root;
+  const uint32_t* __restrict__ pool = a.V.pool;
+  const int T0 = a.V.T0, s0 = a.V.L - a.V.T0, nlev = a.V.nlev;
+  const int sS = a.V.L - (S >= 0 ? S : 0);
+  const uint32_t lim_u = a.V.L >= 32 ? 0xffffffffu : (1u << a.V.L);
+  const uint32_t hmax = (uint32_t)(((1ull << a.V.L) - 1ull) >> 12);
+  int st = 0;
+  uint32_t ph = 0;
+  int ep = 0;
+  for (int64_t t = blockIdx.x; t < ntiles; t += G) {
+    mbar_wait(&full_bar[st], ph);
+    const int64_t p0 = t * RB_TP;
+    const int m = (int)(p0 + RB_TP <= nmain ? RB_TP : nmain - p0);
+    const unsigned char* tile = smem + (size_t)st * STAGE;
+    uint32_t ix[RB_PPT], iy[RB_PPT], val[RB_PPT];
+    float w[RB_PPT];
+    int32_t qv[RB_PPT];
+    uint32_t okm = 0, slowm = 0, fastm = 0;
+    // A. quantise (t = RN(RN(RN(v - o) * inv_side) + 2^32), see rb_point_pass.cu header).
+    //    Every value read from the tile is consumed here, before the slot is
+    //    released to the producer (a pending LDS must not race the refill).
+#pragma unroll
+    for (int j = 0; j < RB_PPT; ++j) {
+      const int pi = ct + j * RB_CONS;
+      const bool in = pi < m;
+      double x, y;
+      if (XY == 0) {
+        const double2 v2 = ((const double2*)tile)[in ? pi : 0];
+        x = v2.x; y = v2.y;
+      } else {
+        const float2 v2 = ((const float2*)tile)[in ? pi : 0];
+        x = (double)v2.x; y = (double)v2.y;
+      }
+      w[j] = ATTR ? ((const float*)(tile + XY_TILE))[in ? pi : 0] : 0.f;
+#if RB_DEBUG_CHECK
+      if (in) {
+        const double gx = XY == 0 ? ((const double*)a.xy)[2 * (p0 + pi)] : (double)((const float*)a.xy)[2 * (p0 + pi)];
+        const float gw = ATTR ? a.attr[p0 + pi] : 0.f;
+        if (gx != x) atomicAdd((unsigned long long*)a.gcnt, 1ull);
+        if (ATTR && gw != w[j]) atomicAdd((unsigned long long*)a.gcnt + 1, 1ull);
+      }
+#endif
+      const double tx = __dadd_rn(__dmul_rn(__dsub_rn(x, ox), inv_side), 4294967296.0);
+      const double ty = __dadd_rn(__dmul_rn(__dsub_rn(y, oy), inv_side), 4294967296.0);
+      const uint32_t lx = (uint32_t)__double2loint(tx), hx = (uint32_t)__double2hiint(tx);
+      const uint32_t ly = (uint32_t)__double2loint(ty), hy = (uint32_t)__double2hiint(ty);
+      ix[j] = __funnelshift_r(lx, hx, 20);
+      iy[j] = __funnelshift_r(ly, hy, 20);
+      const bool good = ((hx - 0x41F00000u) <= hmax) & ((hy - 0x41F00000u) <= hmax) &
+                        (((lx + 2u) & 0xffffcu) != 0u) & (((ly + 2u) & 0xffffcu) != 0u) & (ix[j] < lim_u) &
+                        (iy[j] < lim_u);
+      okm |= (in & good) ? (1u << j) : 0u;
+      slowm |= (in & !good) ? (1u << j) : 0u;
+      qv[j] = 0;
+      if (ATTR) {
+        const float aw = fabsf(w[j]);
+        fastm |= ((aw < wmax) & ((aw >= wmin) | (aw == 0.f)) & !RB_DEBUG_SLOWSUM) ? (1u << j) : 0u;
+        qv[j] = __float2int_rn(w[j] * sc);
+      }
+    }
+#if !RB_LATE_RELEASE
+    // WAR hazard across proxies: an mbarrier arrive does not wait for LDS
+    // still in flight, so order this warp's generic-proxy reads of the slot
+    // before the async-proxy (bulk copy) refill that the arrive enables.
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if ((ct & 31) == 0) mbar_arrive(&empty_bar[st]);  // slot may be refilled
+    if (++st == RB_NST) { st = 0; ph ^= 1u; }
+#endif
+    if (slowm) {  // rare: exact division + domain check
+#pragma unroll
+      for (int j = 0; j < RB_PPT; ++j) {
+        if (slowm & (1u << j)) {
+          const uint64_t qq = quantize_exact(a.xy, p0 + ct + j * RB_CONS, XY, ox, oy, a.side, a.lim, a.first_bad,
+                                             a.idx_base);
+          if (qq != ~0ull) { ix[j] = (uint32_t)qq; iy[j] = (uint32_t)(qq >> 32); okm |= 1u << j; }
+        }
+      }
+    }
+    // B. summary in shared memory, then the L2-resident radix table
+#pragma unroll
+    for (int j = 0; j < RB_PPT; ++j) {
+      const bool okj = (okm >> j) & 1u;
+      uint32_t sv = 0xffffu;
+      if (S >= 0) sv = okj ? (uint32_t)summ[((iy[j] >> sS) << S) | (ix[j] >> sS)] : 0u;
+      const uint32_t* rp = root + (((iy[j] >> s0) << T0) | (ix[j] >> s0));
+      val[j] = ldg_pred(rp, okj & (sv == 0xffffu), okj ? sv : 0u);
+    }
+    // C. node levels (ACT descent), warp-uniform skip
+    uint32_t anyn = 0;
+#pragma unroll
+    for (int j = 0; j < RB_PPT; ++j) anyn |= val[j];
+    if (__any_sync(0xffffffffu, (anyn & RB_VALUE_NODE) != 0u)) {
+      int s = s0;
+#pragma unroll 1
+      for (int li = 0; li < nlev; ++li) {
+        const int kk = lv.ks[li];
+        const uint32_t* __restrict__ nodes = lv.nodes[li];
+        s -= kk;
+        const uint32_t msk = (1u << kk) - 1u;
+#pragma unroll
+        for (int j = 0; j < RB_PPT; ++j) {
+          const bool nd = (val[j] & RB_VALUE_NODE) != 0u;
+          const uint32_t slot = (((iy[j] >> s) & msk) << kk) | ((ix[j] >> s) & msk);
+          const uint32_t* np = nodes + (((val[j] & RB_VALUE_PAYLOAD) << (2 * kk)) + slot);
+          val[j] = ldg_pred(np, nd, val[j]);
+        }
+      }
+    }
+    // D. common case inline: one interior owner and an in-window attribute
+    uint32_t rarem = 0;
+#pragma unroll
+    for (int j = 0; j < RB_PPT; ++j) {
+      const uint32_t v = val[j];
+      const bool fast = !ATTR || ((fastm >> j) & 1u);
+      const uint32_t sv = v - 1u;
+      const bool common = (v != 0u) & ((sv & (RB_VALUE_LIST | 1u)) == 0u) & fast;
+      if (common) h.add_fast(sv, qv[j]);
+      rarem |= (!common & (v != 0u)) ? (1u << j) : 0u;
+    }
+    // E. boundary owners, owner lists, out-of-window attributes
+    if (rarem) {
+#pragma unroll
+      for (int j = 0; j < RB_PPT; ++j) {
+        if (rarem & (1u << j)) {
+          const bool fast = !ATTR || ((fastm >> j) & 1u);
+          add_owners_i<ATTR>(h, pool, val[j], w[j], qv[j], fast);
+        }
+      }
+    }
+#if RB_LATE_RELEASE
+    __syncwarp();
+    if ((ct & 31) == 0) mbar_arrive(&empty_bar[st]);
+    if (++st == RB_NST) { st = 0; ph ^= 1u; }
+#endif
+    if (ATTR && ++ep == 65536 / RB_TP) {  // fold the 16-bit fixed-point halves every 65536 points
+      ep = 0;
+      asm volatile("bar.sync 1, %0;" ::"r"(RB_CONS) : "memory");
+      for (int q = ct; q < R2; q += RB_CONS) {
+        acc[q] += ((long long)(int32_t)h3[3 * q + 2] << 16) + (long long)h3[3 * q + 1];
+        h3[3 * q + 1] = 0;
+        h3[3 * q + 2] = 0;
+      }
+      asm volatile("bar.sync 1, %0;" ::"r"(RB_CONS) : "memory");
+    }
+  }
+  // up to 3 trailing points (n not a multiple of 4): CTA 0, float64 path
+  if (blockIdx.x == 0 && ct < (int)(a.n - nmain)) {
+    const int64_t i = nmain + ct;
+    const uint64_t qq = quantize_exact(a.xy, i, XY, ox, oy, a.side, a.lim, a.first_bad, a.idx_base);
+    if (qq != ~0ull) {
+      const uint32_t v = index_lookup(a.V, (uint32_t)qq, (uint32_t)(qq >> 32));
+      if (v != 0u) add_owners_i<ATTR>(h, pool, v, ATTR ? a.attr[i] : 0.f, 0, false);
+    }
+  }
+  asm volatile("bar.sync 1, %0;" ::"r"(RB_CONS) : "memory");
+  uint32_t* pc = a.part_cnt + (size_t)blockIdx.x * R2;
+  long long* pa = a.part_acc + (size_t)blockIdx.x * R2;
+  double* ps = a.part_sum + (size_t)blockIdx.x * R2;
+  for (int q = ct; q < R2; q += RB_CONS) {
+    pc[q] = h3[ATTR ? 3 * q : q];
+    if (ATTR) {
+      pa[q] = acc[q] + ((long long)(int32_t)h3[3 * q + 2] << 16) + (long long)h3[3 * q + 1];
+      ps[q] = slow[q];
+    }
+  }
+}
+
+// binary scale of the SUM fixed point from a strided sample of the attribute
+__global__ void k_attr_scale(const float* attr, int64_t n, int* scale_exp) {
+  __shared__ float red[256];
+  float m = 0.f;
+  const int64_t stride = n / 4096 > 0 ? n / 4096 : 1;
+  for (int64_t k = threadIdx.x; k < 4096 && k * stride < n; k += blockDim.x) {
+    const float v = fabsf(attr[k * stride]);
+    if (isfinite(v)) m = fmaxf(m, v);
+  }
+  red[threadIdx.x] = m;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] = fmaxf(red[threadIdx.x], red[threadIdx.x + o]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    int e = 0;
+    int S = 0;
+    if (red[0] > 0.f) {
+      frexpf(red[0], &e);  // red[0] < 2^e
+      S = 29 - e;          // fast window [2^(e-9), 2^(e+1))
+    }
+    S = S < -96 ? -96 : (S > 126 ? 126 : S);
+    *scale_exp = S;
+  }
+}
+
+// deterministic reduction of the fixed-point rows (fixed CTA order)
+__global__ void k_reduce_fixed(const uint32_t* part_cnt, const long long* part_acc, const double* part_sum, int nrows,
+                               int R2, bool attr, const int* scale_exp, int64_t* cnt_out, double* sum_out) {
+  const int S = attr ? *scale_exp : 0;
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < R2; q += gridDim.x * blockDim.x) {
     uint64_t c = 0;
+    long long f = 0;
     double s = 0.0;
     for (int r = 0; r < nrows; ++r) {
       c += part_cnt[(size_t)r * R2 + q];
-      if (attr) s += part_sum[(size_t)r * R2 + q];
+      if (attr) { f += part_acc[(size_t)r * R2 + q]; s += part_sum[(size_t)r * R2 + q]; }
     }
-    if (accumulate) { cnt_out[q] += (int64_t)c; sum_out[q] += s; }
-    else { cnt_out[q] = (int64_t)c; sum_out[q] = s; }
+    cnt_out[q] += (int64_t)c;
+    if (attr) sum_out[q] += ldexp((double)f, -S) + s;
   }
 }
 
@@ -226,7 +918,7 @@ __global__ void k_init_out(int64_t* cnt_out, double* sum_out, int R2, int flags,
 
 template <int XY, bool SMEM, bool ATTR, bool VEC>
 static cudaError_t launch_t(const PassArgs& a, int blocks, size_t smem, cudaStream_t s) {
-  auto kern = k_point_pass<XY, SMEM, ATTR, VEC>;
+  auto kern = k_point_pass_global<XY, SMEM, ATTR, VEC>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -248,6 +940,64 @@ static cudaError_t launch_a(const PassArgs& a, bool vec, int blocks, size_t smem
 
 static int g_num_sms = 0;
 
+static void pool_keep_warm() {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  });
+}
+
+// largest region count whose histogram (28 B per bin pair entry) fits the
+// 200 KB shared-memory budget of one CTA
+#define RB_SMEM_BUDGET (200 * 1024)
+
+template <int XY, bool ATTR, bool VEC>
+static cudaError_t launch_smem(const PassArgs& a, size_t smem, cudaStream_t s, int* blocks_out) {
+  auto kern = k_point_pass<XY, ATTR, VEC>;
+  static int cached_blocks = -1;
+  static size_t cached_smem = 0;
+  if (cached_blocks < 0 || cached_smem != smem) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, RB_SMEM_BUDGET);
+    if (e) return e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem);
+    if (e) return e;
+    cached_blocks = std::max(1, per_sm) * g_num_sms;
+    cached_smem = smem;
+  }
+  *blocks_out = cached_blocks;
+  return cudaSuccess;
+}
+template <int XY, bool ATTR>
+static cudaError_t launch_tma(size_t smem, int* blocks_out) {
+  auto kern = k_point_pass_tma<XY, ATTR>;
+  static int cached_blocks = -1;
+  static size_t cached_smem = 0;
+  if (cached_blocks < 0 || cached_smem != smem) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, RB_SMEM_BUDGET);
+    if (e) return e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, RB_CONS + 32, smem);
+    if (e) return e;
+    cached_blocks = std::max(1, per_sm) * g_num_sms;
+    cached_smem = smem;
+  }
+  *blocks_out = cached_blocks;
+  return cudaSuccess;
+}
+
+template <int XY, bool ATTR, bool VEC>
+static cudaError_t run_smem(const PassArgs& a, int blocks, size_t smem, cudaStream_t s) {
+  k_point_pass<XY, ATTR, VEC><<<blocks, 256, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
 // flags: bit0 = zero the outputs first, bit1 = reset first_bad first
 int point_pass(const rb_approx* A, const void* xy, int32_t dtype, int64_t n, const float* attr, int64_t* cnt_out,
                double* sum_out, int64_t* first_bad, int flags, int64_t idx_base, cudaStream_t s) {
@@ -256,6 +1006,7 @@ int point_pass(const rb_approx* A, const void* xy, int32_t dtype, int64_t n, con
     RB_CUDA(cudaGetDevice(&dev));
     RB_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
   }
+  pool_keep_warm();
   const int R2 = 2 * A->n_regions;
   PassArgs a{};
   a.V = A->view();
@@ -273,35 +1024,89 @@ int point_pass(const rb_approx* A, const void* xy, int32_t dtype, int64_t n, con
   a.gcnt = (unsigned long long*)cnt_out;
   a.gsum = sum_out;
   a.idx_base = idx_base;
-  const bool smem_hist = (size_t)R2 * 12 <= 96 * 1024;
-  const size_t smem = smem_hist ? (size_t)R2 * 12 : 0;
-  bool vec = ((uintptr_t)xy % 32 == 0) && (!attr || (uintptr_t)attr % (dtype == RB_XY_F64 ? 8 : 16) == 0);
-  int per_sm = smem_hist ? std::max(1, std::min(4, (int)((200 * 1024) / std::max<size_t>(smem, 1)))) : 4;
-  int blocks = g_num_sms * per_sm;
+  const size_t per_bin = attr ? 28 : 4;
+  const bool smem_hist = (size_t)R2 * per_bin <= RB_SMEM_BUDGET;
+  const size_t smem = smem_hist ? (size_t)R2 * per_bin : 0;
+  const bool vec = ((uintptr_t)xy % 32 == 0) && (!attr || (uintptr_t)attr % (dtype == RB_XY_F64 ? 8 : 16) == 0);
   if (flags) {
     k_init_out<<<std::max(1, (R2 + 255) / 256), 256, 0, s>>>(cnt_out, sum_out, R2, flags, a.first_bad);
     RB_CUDA(cudaGetLastError());
     ++g_launches;
   }
   if (n == 0) return RB_OK;
-  void* scratch = nullptr;
-  if (smem_hist) {
-    size_t bytes = (size_t)blocks * R2 * (4 + (attr ? 8 : 0));
-    RB_CUDA(cudaMallocAsync(&scratch, bytes, s));
-    a.part_cnt = (uint32_t*)scratch;
-    a.part_sum = (double*)((char*)scratch + (size_t)blocks * R2 * 4);
-  }
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  if (!smem_hist) {
+    int blocks = g_num_sms * 4;
+    if (g_timing) {
+      RB_CUDA(cudaEventCreate(&ev0));
+      RB_CUDA(cudaEventCreate(&ev1));
+      RB_CUDA(cudaEventRecord(ev0, s));
+    }
+    cudaError_t e = dtype == RB_XY_F64 ? launch_a<0, false>(a, vec, blocks, 0, s) : launch_a<1, false>(a, vec, blocks, 0, s);
+    if (e) return cuda_fail(e, "k_point_pass_global");
+    ++g_launches;
+    if (g_timing) {
+      RB_CUDA(cudaEventRecord(ev1, s));
+      std::lock_guard<std::mutex> lk(g_ev_mu);
+      g_events.emplace_back(ev0, ev1);
+    }
+    return RB_OK;
+  }
+  int blocks = 0;
+  cudaError_t e;
+  const size_t summ_bytes = A->S >= 0 ? ((size_t)2 << (2 * A->S)) + 32 : 0;
+  static const bool no_tma = getenv("RB_NO_TMA") != nullptr;
+  const bool tma = !no_tma && ((uintptr_t)xy % 16 == 0) && (!attr || (uintptr_t)attr % 16 == 0) &&
+                   (size_t)RB_NST * RB_TP * ((dtype == RB_XY_F64 ? 16 : 8) + (attr ? 4 : 0)) + smem + summ_bytes <=
+                       RB_SMEM_BUDGET;
+#define RB_DISPATCH(FN, ...)                                                                          \
+  if (dtype == RB_XY_F64) {                                                                           \
+    if (attr) e = vec ? FN<0, true, true>(__VA_ARGS__) : FN<0, true, false>(__VA_ARGS__);             \
+    else e = vec ? FN<0, false, true>(__VA_ARGS__) : FN<0, false, false>(__VA_ARGS__);                \
+  } else {                                                                                            \
+    if (attr) e = vec ? FN<1, true, true>(__VA_ARGS__) : FN<1, true, false>(__VA_ARGS__);             \
+    else e = vec ? FN<1, false, true>(__VA_ARGS__) : FN<1, false, false>(__VA_ARGS__);                \
+  }
+  size_t tma_smem = 0;
+  if (tma) {
+    tma_smem = (size_t)RB_NST * RB_TP * ((dtype == RB_XY_F64 ? 16 : 8) + (attr ? 4 : 0)) + smem + summ_bytes;
+    e = dtype == RB_XY_F64 ? (attr ? launch_tma<0, true>(tma_smem, &blocks) : launch_tma<0, false>(tma_smem, &blocks))
+                           : (attr ? launch_tma<1, true>(tma_smem, &blocks) : launch_tma<1, false>(tma_smem, &blocks));
+  } else {
+    RB_DISPATCH(launch_smem, a, smem, s, &blocks);
+  }
+  if (e) return cuda_fail(e, "k_point_pass setup");
+  void* scratch = nullptr;
+  const size_t rows = (size_t)blocks * R2;
+  RB_CUDA(cudaMallocAsync(&scratch, rows * (4 + 8 + 8) + 16, s));
+  a.part_acc = (long long*)scratch;
+  a.part_sum = (double*)((char*)scratch + rows * 8);
+  a.part_cnt = (uint32_t*)((char*)scratch + rows * 16);
+  int* scale = (int*)((char*)scratch + rows * 20);
+  a.scale_exp = scale;
+  if (attr) {
+    k_attr_scale<<<1, 256, 0, s>>>(attr, n, scale);
+    RB_CUDA(cudaGetLastError());
+    ++g_launches;
+  }
   if (g_timing) {
     RB_CUDA(cudaEventCreate(&ev0));
     RB_CUDA(cudaEventCreate(&ev1));
     RB_CUDA(cudaEventRecord(ev0, s));
   }
-  cudaError_t e;
-  if (dtype == RB_XY_F64)
-    e = smem_hist ? launch_a<0, true>(a, vec, blocks, smem, s) : launch_a<0, false>(a, vec, blocks, smem, s);
-  else
-    e = smem_hist ? launch_a<1, true>(a, vec, blocks, smem, s) : launch_a<1, false>(a, vec, blocks, smem, s);
+  if (tma) {
+    if (dtype == RB_XY_F64) {
+      if (attr) k_point_pass_tma<0, true><<<blocks, RB_CONS + 32, tma_smem, s>>>(a);
+      else k_point_pass_tma<0, false><<<blocks, RB_CONS + 32, tma_smem, s>>>(a);
+    } else {
+      if (attr) k_point_pass_tma<1, true><<<blocks, RB_CONS + 32, tma_smem, s>>>(a);
+      else k_point_pass_tma<1, false><<<blocks, RB_CONS + 32, tma_smem, s>>>(a);
+    }
+    e = cudaGetLastError();
+  } else {
+    RB_DISPATCH(run_smem, a, blocks, smem, s);
+  }
+#undef RB_DISPATCH
   if (e) return cuda_fail(e, "k_point_pass");
   ++g_launches;
   if (g_timing) {
@@ -309,13 +1114,11 @@ int point_pass(const rb_approx* A, const void* xy, int32_t dtype, int64_t n, con
     std::lock_guard<std::mutex> lk(g_ev_mu);
     g_events.emplace_back(ev0, ev1);
   }
-  if (smem_hist) {
-    k_reduce_rows<<<std::max(1, (R2 + 255) / 256), 256, 0, s>>>(a.part_cnt, a.part_sum, blocks, R2, attr != nullptr,
-                                                                1, cnt_out, sum_out);
-    RB_CUDA(cudaGetLastError());
-    ++g_launches;
-    RB_CUDA(cudaFreeAsync(scratch, s));
-  }
+  k_reduce_fixed<<<std::max(1, (R2 + 255) / 256), 256, 0, s>>>(a.part_cnt, a.part_acc, a.part_sum, blocks, R2,
+                                                               attr != nullptr, scale, cnt_out, sum_out);
+  RB_CUDA(cudaGetLastError());
+  ++g_launches;
+  RB_CUDA(cudaFreeAsync(scratch, s));
   return RB_OK;
 }
 

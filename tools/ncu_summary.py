@@ -1,0 +1,69 @@
+"""Summarise an ncu report: key metrics, stall breakdown, instruction mix, top stalled SASS.
+usage: python tools/ncu_summary.py report.ncu-rep [points] [json_out]"""
+import csv
+import io
+import json
+import subprocess
+import sys
+from collections import Counter
+
+rep = sys.argv[1]
+npts = float(sys.argv[2]) if len(sys.argv) > 2 else 0
+out_json = sys.argv[3] if len(sys.argv) > 3 else None
+
+
+def ncu(*args):
+    return subprocess.run(["ncu", "-i", rep, *args], capture_output=True, text=True).stdout
+
+
+det = list(csv.reader(io.StringIO(ncu("--page", "details", "--csv"))))
+h = det[0]
+keep = ("Duration", "DRAM Throughput", "Memory Throughput", "L1/TEX Cache Throughput", "L2 Cache Throughput",
+        "Compute (SM) Throughput", "Issue Slots Busy", "Warp Cycles Per Issued Instruction",
+        "Achieved Active Warps Per SM", "L2 Hit Rate", "Registers Per Thread", "Grid Size", "Block Size",
+        "Executed Ipc Active", "Avg. Active Threads Per Warp", "Theoretical Occupancy", "SM Frequency")
+summary = {}
+for row in det[1:]:
+    d = dict(zip(h, row))
+    if d.get("Metric Name") in keep and d.get("Metric Name") not in summary:
+        summary[d["Metric Name"]] = (d.get("Metric Value"), d.get("Metric Unit"))
+raw = list(csv.reader(io.StringIO(ncu("--page", "raw", "--csv"))))
+rh, ru, rv = raw[0], raw[1], raw[2]
+rawd = dict(zip(rh, rv))
+for k in ("dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_sector_hit_rate.pct", "gpu__time_duration.sum"):
+    if k in rawd:
+        summary[k] = (rawd[k], ru[rh.index(k)])
+for k, (v, u) in summary.items():
+    print(f"{k:40s} {v} {u}")
+src = list(csv.reader(io.StringIO(ncu("--page", "source", "--csv", "--print-source", "sass"))))
+sh = src[1]
+data = [dict(zip(sh, r)) for r in src[2:]]
+cols = [c for c in sh if c.startswith("stall_") and "Not Issued" not in c]
+tot = {c: sum(float(d[c] or 0) for d in data) for c in cols}
+T = sum(tot.values()) or 1
+print("-- stall breakdown")
+for c, v in sorted(tot.items(), key=lambda x: -x[1])[:8]:
+    print(f"  {c:26s} {v / T * 100:5.1f}%")
+cnt = Counter()
+for d in data:
+    ex = float(d["Instructions Executed"] or 0)
+    toks = d["Source"].split()
+    if not toks:
+        continue
+    op = toks[1] if toks[0].startswith("@") and len(toks) > 1 else toks[0]
+    cnt[op.split(".")[0]] += ex
+E = sum(cnt.values())
+if npts:
+    print(f"-- {E * 32 / npts:.1f} thread-instructions per point")
+    for k, v in cnt.most_common(16):
+        print(f"  {k:10s} {v * 32 / npts:6.2f}/pt")
+key = "Warp Stall Sampling (All Samples)"
+S = sum(float(d[key] or 0) for d in data) or 1
+print("-- top stalled instructions")
+for d in sorted(data, key=lambda d: -float(d[key] or 0))[:12]:
+    print(f"  {float(d[key]) / S * 100:5.1f}%  {d['Source'][:90]}")
+if out_json:
+    dr = float(rawd.get("dram__bytes_read.sum", 0) or 0) + float(rawd.get("dram__bytes_write.sum", 0) or 0)
+    with open(out_json, "w") as f:
+        json.dump({"report": rep, "metrics": {k: v for k, (v, u) in summary.items()},
+                   "dram_bytes_per_launch": dr, "stalls": {k: v / T for k, v in tot.items()}}, f, indent=1)
