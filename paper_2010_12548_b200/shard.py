@@ -1,0 +1,30 @@
+"""Multi-GPU sharding of the point pass (north star subsystem 4).
+
+Points are independent, so the path shards by contiguous point
+ranges (or per-rank batches); the approximation is built deterministically
+on every rank and the per-region [R,2] int64 COUNT and float64
+SUM partials are combined with ONE all-reduce per tensor (NCCL over NVLink on
+the B200 box, gloo in CPU tests).  Counts are exact in int64; float64 sums
+differ from a 1-GPU run only by summation order (rel < 1e-12).
+"""
+from __future__ import annotations
+
+
+def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous, balanced [begin, end) slice of n points for `rank`."""
+    if world <= 0 or not (0 <= rank < world):
+        raise ValueError("bad rank/world")
+    return n * rank // world, n * (rank + 1) // world
+
+
+def combine(cnt, sm, group=None):
+    """In-place all-reduce (sum) of the per-region partials of every rank."""
+    import torch.distributed as dist
+
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(cnt, op=dist.ReduceOp.SUM, group=group)
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM, group=group)
+    return cnt, sm
+
+
+__all__ = ["shard_range", "combine"]
