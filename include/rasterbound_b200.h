@@ -125,6 +125,11 @@ int rb_index_from_cells(const rb_grid* grid, int64_t n_cells, const int32_t* cov
                         const uint64_t* code, const uint8_t* kind, const int32_t* cov_region, int64_t n_cov,
                         int32_t n_regions, const rb_build_opts* opts, void* stream, rb_approx** out);
 int rb_approx_stats(const rb_approx* a, rb_stats* out);
+/* Mark up to 4095 frequently hit regions (device or host int32 array) whose
+ * alpha COUNT/SUM the point pass privatises in shared memory when the full
+ * per-region histogram does not fit there (large region sets, e.g. 40,000
+ * census blocks).  Results are unchanged.  Requires n_regions < 2^17 - 1. */
+int rb_approx_set_hot(rb_approx* a, const int32_t* regions, int32_t n_hot, void* stream);
 void rb_approx_free(rb_approx* a);
 
 /* query.join_act point loop: per region alpha/beta COUNT and

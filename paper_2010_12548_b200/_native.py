@@ -22,13 +22,15 @@ MODE_CONSERVATIVE, MODE_CENTER_SAMPLED = 0, 1
 LAYOUT_DENSE, LAYOUT_TRIE = 0, 1
 XY_F64, XY_F32 = 0, 1
 VALUE_LIST = 0x40000000
+CODE_MASK = 0x3FFFF
+MAX_HOT = 4095
 VALUE_PAYLOAD = 0x3FFFFFFF
 
 # every symbol include/rasterbound_b200.h declares
 EXPORTS = (
     "rb_version", "rb_last_error", "rb_level_for_bound", "rb_approx_build", "rb_approx_stats", "rb_approx_free",
     "rb_point_pass", "rb_join_host", "rb_lookup", "rb_owner_pool", "rb_point_cells", "rb_approx_cells",
-    "rb_approx_partial", "rb_exact_pip", "rb_exact_distance", "rb_index_from_cells", "rb_instrument",
+    "rb_approx_partial", "rb_exact_pip", "rb_exact_distance", "rb_index_from_cells", "rb_instrument", "rb_approx_set_hot",
 )
 
 
@@ -90,6 +92,7 @@ def load() -> C.CDLL:
     L.rb_exact_pip.argtypes = [C.POINTER(Polygons), p, p, p, i64, p, p]
     L.rb_exact_distance.argtypes = [C.POINTER(Polygons), p, p, p, i64, p, p]
     L.rb_instrument.argtypes = [i32, C.POINTER(i64), C.POINTER(i64), C.POINTER(d)]
+    L.rb_approx_set_hot.argtypes = [p, p, i32, p]
     for name in EXPORTS:
         getattr(L, name)  # AttributeError if an export is missing
     _lib = L

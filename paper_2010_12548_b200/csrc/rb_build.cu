@@ -21,6 +21,10 @@
 
 #include "rb_internal.cuh"
 
+#ifndef RB_SUMMARY_DEFAULT
+#define RB_SUMMARY_DEFAULT 7
+#endif
+
 namespace rb {
 
 // ------------------------------------------------------------ CUB helpers
@@ -534,7 +538,7 @@ __global__ void k_pos_values(Recs r, int64_t n, const int64_t* pbeg, int64_t npo
       pval[P] = (uint32_t)((((uint32_t)r.region[b] << 1) | (r.kind[b] == RB_KIND_B ? 1u : 0u)) + 1u);
     } else {
       int64_t w = poff[P];
-      pool[w++] = (uint32_t)nown[P];
+      pool[w++] = RB_POOL_COUNT_FLAG | (uint32_t)nown[P];
       for (int64_t k = b; k < e; ++k)
         if (k == b || r.region[k] != r.region[k - 1])
           pool[w++] = ((uint32_t)r.region[k] << 1) | (r.kind[k] == RB_KIND_B ? 1u : 0u);
@@ -906,7 +910,7 @@ static int index_impl(int L, int64_t total_cells, const int32_t* cp_in, const ui
   A->stats.n_nodes = total_nodes;
   // summary table for the shared-memory fast path (owner values must fit u16)
   {
-    int Smax = 7;
+    int Smax = RB_SUMMARY_DEFAULT;
     if (const char* e = getenv("RB_SUMMARY_LEVEL")) Smax = atoi(e);
     A->S = -1;
     if (Smax >= 0 && 2 * (int64_t)A->n_regions + 1 < 0xffff) {
@@ -1260,5 +1264,74 @@ extern "C" int rb_index_from_cells(const rb_grid* grid, int64_t n_cells, const i
   if (st != RB_OK) return st;
   A->stats.build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
   *out = A.release();
+  return RB_OK;
+}
+
+namespace rb {
+__global__ void k_hot_remap(const int32_t* regions, int32_t K, int32_t* remap) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < K; k += gridDim.x * blockDim.x) remap[regions[k]] = k + 1;
+}
+// annotate single-owner values (root / nodes) with their region's hot slot
+__global__ void k_hot_values(uint32_t* v, int64_t n, const int32_t* remap) {
+  GRID_STRIDE(k, n) {
+    const uint32_t x = v[k];
+    if (x == 0u || (x & (RB_VALUE_NODE | RB_VALUE_LIST))) continue;
+    const uint32_t code = x & RB_CODE_MASK;
+    const uint32_t r = (code - 1u) >> 1;
+    v[k] = code | ((uint32_t)remap[r] << RB_HOT_SHIFT);
+  }
+}
+// annotate owner-list entries ((region<<1)|boundary); count words are flagged
+__global__ void k_hot_pool(uint32_t* p, int64_t n, const int32_t* remap) {
+  GRID_STRIDE(k, n) {
+    const uint32_t x = p[k];
+    if (x & RB_POOL_COUNT_FLAG) continue;
+    const uint32_t e = x & RB_CODE_MASK;
+    p[k] = e | ((uint32_t)remap[e >> 1] << RB_HOT_SHIFT);
+  }
+}
+}  // namespace rb
+
+// Mark up to 4095 "hot" regions (e.g. the most frequent owners of a point
+// sample): their alpha COUNT/SUM are accumulated in shared memory by the
+// point pass when the full histogram does not fit there.  Results are
+// unchanged; only where the accumulation happens.  Synchronises `stream`.
+extern "C" int rb_approx_set_hot(rb_approx* a, const int32_t* regions, int32_t n_hot, void* stream) {
+  using namespace rb;
+  if (!a) return fail(RB_CONFIG_ERROR, "null approximation");
+  if (a->n_hot) return fail(RB_CONFIG_ERROR, "hot regions already set");
+  if (n_hot < 0 || n_hot > RB_MAX_HOT) return fail(RB_CAPACITY_ERROR, "at most 4095 hot regions");
+  if ((int64_t)a->n_regions >= ((int64_t)1 << 17) - 1) return fail(RB_CAPACITY_ERROR, "hot slots need < 2^17 regions");
+  if (n_hot == 0) return RB_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  std::vector<int32_t> h(n_hot);
+  RB_CUDA(cudaMemcpyAsync(h.data(), regions, n_hot * 4, cudaMemcpyDefault, s));
+  RB_CUDA(cudaStreamSynchronize(s));
+  {
+    std::vector<char> seen(a->n_regions, 0);
+    for (int32_t r : h) {
+      if (r < 0 || r >= a->n_regions) return fail(RB_CONFIG_ERROR, "hot region out of range");
+      if (seen[r]++) return fail(RB_CONFIG_ERROR, "duplicate hot region");
+    }
+  }
+  RB_CUDA(a->hot_region.alloc(n_hot * 4));
+  RB_CUDA(cudaMemcpyAsync(a->hot_region.p, h.data(), n_hot * 4, cudaMemcpyHostToDevice, s));
+  DBuf remap;
+  RB_CUDA(remap.alloc((size_t)a->n_regions * 4));
+  RB_CUDA(cudaMemsetAsync(remap.p, 0, (size_t)a->n_regions * 4, s));
+  k_hot_remap<<<nblk(n_hot), 256, 0, s>>>(a->hot_region.as<int32_t>(), n_hot, remap.as<int32_t>());
+  k_hot_values<<<nblk(a->root_entries), 256, 0, s>>>(a->root.as<uint32_t>(), a->root_entries, remap.as<int32_t>());
+  for (size_t i = 0; i < a->node_bufs.size(); ++i) {
+    const int64_t n = (int64_t)(a->node_bufs[i].bytes / 4);
+    k_hot_values<<<nblk(n), 256, 0, s>>>(a->node_bufs[i].as<uint32_t>(), n, remap.as<int32_t>());
+  }
+  if (a->pool_len) k_hot_pool<<<nblk(a->pool_len), 256, 0, s>>>(a->pool.as<uint32_t>(), a->pool_len, remap.as<int32_t>());
+  RB_CUDA(cudaGetLastError());
+  if (a->S >= 0)  // annotated values exceed u16: the summary refers them to the index
+    k_summary<<<nblk(((int64_t)32 << (2 * a->S))), 256, 0, s>>>(a->root.as<uint32_t>(), a->T0, a->S,
+                                                                 a->summary.as<uint16_t>());
+  RB_CUDA(cudaGetLastError());
+  RB_CUDA(cudaStreamSynchronize(s));
+  a->n_hot = n_hot;
   return RB_OK;
 }

@@ -92,7 +92,13 @@ extern "C" int rb_lookup(const rb_approx* a, const void* xy, int32_t xy_dtype, i
 extern "C" int rb_owner_pool(const rb_approx* a, uint32_t* dst, int64_t* n) {
   if (!a || !n) return fail(RB_CONFIG_ERROR, "null argument");
   *n = a->pool_len;
-  if (dst && a->pool_len) RB_CUDA(cudaMemcpy(dst, a->pool.p, a->pool_len * 4, cudaMemcpyDefault));
+  if (dst && a->pool_len) {
+    // public form: count words and (region<<1)|boundary entries, no internal annotations
+    std::vector<uint32_t> h(a->pool_len);
+    RB_CUDA(cudaMemcpy(h.data(), a->pool.p, a->pool_len * 4, cudaMemcpyDeviceToHost));
+    for (auto& x : h) x = (x & RB_POOL_COUNT_FLAG) ? (x & ~RB_POOL_COUNT_FLAG) : (x & RB_CODE_MASK);
+    RB_CUDA(cudaMemcpy(dst, h.data(), a->pool_len * 4, cudaMemcpyDefault));
+  }
   return RB_OK;
 }
 

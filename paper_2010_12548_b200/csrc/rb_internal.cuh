@@ -19,6 +19,14 @@
 
 // TRIE slot tag for "child node" (never returned by rb_lookup).
 #define RB_VALUE_NODE 0x80000000u
+// Hot-slot annotation (rb_approx_set_hot): bits 18..29 of a single-owner
+// value / owner-list entry carry (hot slot + 1); stripped by rb_lookup and
+// rb_owner_pool.  Owner-list count words carry RB_POOL_COUNT_FLAG.
+#define RB_HOT_SHIFT 18
+#define RB_HOT_BITS 0xfffu
+#define RB_CODE_MASK 0x3ffffu
+#define RB_POOL_COUNT_FLAG 0x80000000u
+#define RB_MAX_HOT 4095
 
 namespace rb {
 
@@ -214,6 +222,8 @@ struct rb_approx {
   int T0 = 0, k = 4;
   rb::DBuf summary;  // u16 [4^S] or empty
   int S = -1;
+  rb::DBuf hot_region;  // int32 [n_hot]: hot slot -> region
+  int32_t n_hot = 0;
   // optional exports
   rb::DBuf cell_poly, cell_level, cell_code, cell_kind;
   int64_t n_cells = 0;

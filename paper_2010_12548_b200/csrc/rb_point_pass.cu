@@ -82,6 +82,8 @@ struct PassArgs {
   int64_t idx_base;  // global index of point 0 (chunked host joins)
   long long* part_acc;
   const int* scale_exp;
+  const int32_t* hot_region;  // global mode: hot slot -> region
+  int n_hot;
 };
 
 template <bool SMEM, bool ATTR>
@@ -113,15 +115,15 @@ __device__ __forceinline__ void point(const PassArgs& a, Hist<SMEM, ATTR>& h, do
   if (val == 0) return;
   double w = (double)wf;
   if (!(val & RB_VALUE_LIST)) {
-    uint32_t s = val - 1u;
+    uint32_t s = (val & RB_CODE_MASK) - 1u;
     uint32_t q = s & ~1u;  // 2 * region
     h.add(q, w);
     if (s & 1u) h.add(q + 1, w);
   } else {
     const uint32_t* L = a.V.pool + (val & RB_VALUE_PAYLOAD);
-    uint32_t k = __ldg(L);
+    uint32_t k = __ldg(L) & ~RB_POOL_COUNT_FLAG;
     for (uint32_t e = 1; e <= k; ++e) {
-      uint32_t ent = __ldg(L + e);
+      uint32_t ent = __ldg(L + e) & RB_CODE_MASK;
       uint32_t q = ent & ~1u;
       h.add(q, w);
       if (ent & 1u) h.add(q + 1, w);
@@ -262,46 +264,49 @@ struct SHist {
 // part); stride 3 is coprime with the 32 banks, one base IMAD per update.
 template <bool ATTR>
 struct IHist {
-  uint32_t* h3;
-  double* slow;
-  __device__ __forceinline__ void add_fast(uint32_t q, int32_t qv) {
-    uint32_t* b = h3 + (ATTR ? 3u * q : q);
-    atomicAdd(b, 1u);
+  uint32_t* h3;              // shared bins: count, fixed-point low 16 bits, signed high part
+  double* slow;              // shared float64 sums of out-of-window values (smem mode)
+  unsigned long long* gcnt;  // non-null: global mode (region set beyond shared memory)
+  double* gsum;
+  __device__ __forceinline__ void fixed(uint32_t b, int32_t qv) {
+    uint32_t* p = h3 + (ATTR ? 3u * b : b);
+    atomicAdd(p, 1u);
     if (ATTR) {
-      atomicAdd(b + 1, (uint32_t)qv & 0xffffu);
-      atomicAdd(b + 2, (uint32_t)(qv >> 16));
+      atomicAdd(p + 1, (uint32_t)qv & 0xffffu);
+      atomicAdd(p + 2, (uint32_t)(qv >> 16));
     }
   }
-  __device__ __forceinline__ void add_slow(uint32_t q, float w) {
+  // bin q = 2*region (+1 for beta); slot = hot slot + 1 of the region (global mode)
+  __device__ __forceinline__ void add(uint32_t q, uint32_t slot, float w, int32_t qv, bool fast) {
+    if (gcnt) {
+      if (slot && !(q & 1u) && fast) { fixed(slot - 1u, qv); return; }
+      atomicAdd(&gcnt[q], 1ull);  // REDG.ADD.64
+      if (ATTR) atomicAdd(&gsum[q], (double)w);  // REDG.ADD.F64
+      return;
+    }
+    if (fast) { fixed(q, qv); return; }
     atomicAdd(h3 + (ATTR ? 3u * q : q), 1u);
     if (ATTR) atomicAdd(&slow[q], (double)w);
   }
-  __device__ __forceinline__ void add(uint32_t q, float w, int32_t qv, bool fast) {
-    if (fast) add_fast(q, qv); else add_slow(q, w);
-  }
 };
 
-#ifndef RB_OWNERS_INLINE
-#define RB_OWNERS_ATTR __noinline__
-#else
-#define RB_OWNERS_ATTR __forceinline__
-#endif
 template <bool ATTR>
-__device__ RB_OWNERS_ATTR void add_owners_i(IHist<ATTR> h, const uint32_t* __restrict__ pool, uint32_t v, float w,
+__device__ __noinline__ void add_owners_i(IHist<ATTR> h, const uint32_t* __restrict__ pool, uint32_t v, float w,
                                           int32_t qv, bool fast) {
   if (!(v & RB_VALUE_LIST)) {
-    const uint32_t sv = v - 1u, q = sv & ~1u;
-    h.add(q, w, qv, fast);
-    if (sv & 1u) h.add(q + 1, w, qv, fast);
+    const uint32_t sv = (v & RB_CODE_MASK) - 1u, q = sv & ~1u;
+    h.add(q, v >> RB_HOT_SHIFT, w, qv, fast);
+    if (sv & 1u) h.add(q + 1, 0u, w, qv, fast);
     return;
   }
   const uint32_t* Lp = pool + (v & RB_VALUE_PAYLOAD);
-  const uint32_t kk = __ldg(Lp);
+  const uint32_t kk = __ldg(Lp) & ~RB_POOL_COUNT_FLAG;
   for (uint32_t e = 1; e <= kk; ++e) {
-    const uint32_t ent = __ldg(Lp + e);
+    const uint32_t x = __ldg(Lp + e);
+    const uint32_t ent = x & RB_CODE_MASK;
     const uint32_t q = ent & ~1u;
-    h.add(q, w, qv, fast);
-    if (ent & 1u) h.add(q + 1, w, qv, fast);
+    h.add(q, x >> RB_HOT_SHIFT, w, qv, fast);
+    if (ent & 1u) h.add(q + 1, 0u, w, qv, fast);
   }
 }
 
@@ -345,15 +350,15 @@ template <bool ATTR>
 __device__ __noinline__ void add_owners(SHist<ATTR> h, const uint32_t* __restrict__ pool, uint32_t v, float w,
                                         int32_t qv, bool fast) {
   if (!(v & RB_VALUE_LIST)) {
-    const uint32_t sv = v - 1u, q = sv & ~1u;
+    const uint32_t sv = (v & RB_CODE_MASK) - 1u, q = sv & ~1u;
     h.add(q, w, qv, fast);
-    h.add(q + 1, w, qv, fast);
+    if (sv & 1u) h.add(q + 1, w, qv, fast);
     return;
   }
   const uint32_t* Lp = pool + (v & RB_VALUE_PAYLOAD);
-  const uint32_t kk = __ldg(Lp);
+  const uint32_t kk = __ldg(Lp) & ~RB_POOL_COUNT_FLAG;
   for (uint32_t e = 1; e <= kk; ++e) {
-    const uint32_t ent = __ldg(Lp + e);
+    const uint32_t ent = __ldg(Lp + e) & RB_CODE_MASK;
     const uint32_t q = ent & ~1u;
     h.add(q, w, qv, fast);
     if (ent & 1u) h.add(q + 1, w, qv, fast);
@@ -522,8 +527,8 @@ __global__ void __launch_bounds__(256, RB_MINB) k_point_pass(PassArgs a) {
           fast = (aw < wmax) & ((aw >= wmin) | (aw == 0.f));
           qv = __float2int_rn(w[i] * sc);
         }
-        const uint32_t sv = v - 1u;
-        if (v != 0u && (sv & (RB_VALUE_LIST | 1u)) == 0u) {
+        const uint32_t sv = (v & RB_CODE_MASK) - 1u;
+        if (v != 0u && !(v & RB_VALUE_LIST) && (sv & 1u) == 0u) {
           if (fast) h.add_fast(sv, qv); else h.add_slow(sv, w[i]);
         } else if (v != 0u) {
           add_owners<ATTR>(h, c.pool, v, w[i], qv, fast);
@@ -549,7 +554,7 @@ __global__ void __launch_bounds__(256, RB_MINB) k_point_pass(PassArgs a) {
       const uint32_t v = index_lookup(a.V, qx, qy);
       if (v == 0) continue;
       const float ww = ATTR ? a.attr[i] : 0.f;
-      if (!(v & RB_VALUE_LIST) && !((v - 1u) & 1u)) h.add_slow(v - 1u, ww);
+      if (!(v & RB_VALUE_LIST) && !(((v & RB_CODE_MASK) - 1u) & 1u)) h.add_slow((v & RB_CODE_MASK) - 1u, ww);
       else add_owners<ATTR>(h, c.pool, v, ww, 0, false);
     }
   }
@@ -580,19 +585,10 @@ __global__ void __launch_bounds__(256, RB_MINB) k_point_pass(PassArgs a) {
 #ifndef RB_NST
 #define RB_NST 3       // ring stages
 #endif
-#ifndef RB_LATE_RELEASE
-#define RB_LATE_RELEASE 0
-#endif
-#ifndef RB_DEBUG_CHECK
-#define RB_DEBUG_CHECK 0
-#endif
-#ifndef RB_DEBUG_SLOWSUM
-#define RB_DEBUG_SLOWSUM 0
-#endif
-#ifndef RB_EXPERIMENT
-#define RB_EXPERIMENT 0  // ablations for profiling: 1 no histogram, 2 no index, 3 both ... see tools/
-#endif
+#ifndef RB_CONS
 #define RB_CONS 256    // consumer threads
+#endif
+#define RB_MINB_TMA (RB_CONS >= 512 ? 1 : 2)
 #define RB_PPT (RB_TP / RB_CONS)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -620,8 +616,8 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
-template <int XY, bool ATTR>
-__global__ void __launch_bounds__(RB_CONS + 32, 2) k_point_pass_tma(PassArgs a) {
+template <int XY, bool ATTR, bool GH = false>
+__global__ void __launch_bounds__(RB_CONS + 32, RB_MINB_TMA) k_point_pass_tma(PassArgs a) {
   constexpr int PB_BYTES = XY == 0 ? 16 : 8;
   constexpr uint32_t XY_TILE = RB_TP * PB_BYTES;
   constexpr uint32_t AT_TILE = ATTR ? RB_TP * 4 : 0;
@@ -631,18 +627,22 @@ __global__ void __launch_bounds__(RB_CONS + 32, 2) k_point_pass_tma(PassArgs a) 
   __shared__ __align__(8) uint64_t full_bar[RB_NST], empty_bar[RB_NST];
   const int R2 = a.R2;
   // layout: [ring][h3: R2*(ATTR?3:1) u32][acc: R2 i64][slow: R2 f64][summary u16]
+  // smem mode: all R2 bins [h3 | acc | slow]; global mode: the n_hot hot alpha bins only
+  const int NB = GH ? a.n_hot : R2;
   unsigned char* hist = smem + (size_t)RB_NST * STAGE;
   uint32_t* h3 = (uint32_t*)hist;
-  const size_t h3_bytes = (((size_t)R2 * (ATTR ? 12 : 4)) + 15) & ~(size_t)15;
+  const size_t h3_bytes = (((size_t)NB * (ATTR ? 12 : 4)) + 15) & ~(size_t)15;
   long long* acc = (long long*)(hist + h3_bytes);
-  double* slow = (double*)(hist + h3_bytes + (ATTR ? (size_t)R2 * 8 : 0));
-  uint16_t* summ = (uint16_t*)(hist + h3_bytes + (ATTR ? (size_t)R2 * 16 : 0));
-  IHist<ATTR> h{h3, slow};
+  double* slow = (double*)(hist + h3_bytes + (ATTR && !GH ? (size_t)R2 * 8 : 0));
+  uint16_t* summ = (uint16_t*)(hist + h3_bytes + (ATTR && !GH ? (size_t)R2 * 16 : 0));
+  IHist<ATTR> h{h3, slow, GH ? a.gcnt : nullptr, GH ? a.gsum : nullptr};
   const int tid = threadIdx.x;
   const int S = a.V.S;
-  for (int q = tid; q < R2 * (ATTR ? 3 : 1); q += blockDim.x) h3[q] = 0;
-  if (ATTR)
+  for (int q = tid; q < NB * (ATTR ? 3 : 1); q += blockDim.x) h3[q] = 0;
+  if (ATTR && !GH)
     for (int q = tid; q < R2; q += blockDim.x) { acc[q] = 0; slow[q] = 0.0; }
+  if (ATTR && GH)
+    for (int q = tid; q < NB; q += blockDim.x) a.part_acc[(size_t)blockIdx.x * NB + q] = 0;
   if (S >= 0) {
     const int nsum = 1 << (2 * S);
     const uint4* src = (const uint4*)a.V.summary;
@@ -731,14 +731,6 @@ __global__ void __launch_bounds__(RB_CONS + 32, 2) k_point_pass_tma(PassArgs a) 
         x = (double)v2.x; y = (double)v2.y;
       }
       w[j] = ATTR ? ((const float*)(tile + XY_TILE))[in ? pi : 0] : 0.f;
-#if RB_DEBUG_CHECK
-      if (in) {
-        const double gx = XY == 0 ? ((const double*)a.xy)[2 * (p0 + pi)] : (double)((const float*)a.xy)[2 * (p0 + pi)];
-        const float gw = ATTR ? a.attr[p0 + pi] : 0.f;
-        if (gx != x) atomicAdd((unsigned long long*)a.gcnt, 1ull);
-        if (ATTR && gw != w[j]) atomicAdd((unsigned long long*)a.gcnt + 1, 1ull);
-      }
-#endif
       const double tx = __dadd_rn(__dmul_rn(__dsub_rn(x, ox), inv_side), 4294967296.0);
       const double ty = __dadd_rn(__dmul_rn(__dsub_rn(y, oy), inv_side), 4294967296.0);
       const uint32_t lx = (uint32_t)__double2loint(tx), hx = (uint32_t)__double2hiint(tx);
@@ -753,11 +745,10 @@ __global__ void __launch_bounds__(RB_CONS + 32, 2) k_point_pass_tma(PassArgs a) 
       qv[j] = 0;
       if (ATTR) {
         const float aw = fabsf(w[j]);
-        fastm |= ((aw < wmax) & ((aw >= wmin) | (aw == 0.f)) & !RB_DEBUG_SLOWSUM) ? (1u << j) : 0u;
+        fastm |= ((aw < wmax) & ((aw >= wmin) | (aw == 0.f))) ? (1u << j) : 0u;
         qv[j] = __float2int_rn(w[j] * sc);
       }
     }
-#if !RB_LATE_RELEASE
     // WAR hazard across proxies: an mbarrier arrive does not wait for LDS
     // still in flight, so order this warp's generic-proxy reads of the slot
     // before the async-proxy (bulk copy) refill that the arrive enables.
@@ -765,7 +756,6 @@ __global__ void __launch_bounds__(RB_CONS + 32, 2) k_point_pass_tma(PassArgs a) 
     __syncwarp();
     if ((ct & 31) == 0) mbar_arrive(&empty_bar[st]);  // slot may be refilled
     if (++st == RB_NST) { st = 0; ph ^= 1u; }
-#endif
     if (slowm) {  // rare: exact division + domain check
 #pragma unroll
       for (int j = 0; j < RB_PPT; ++j) {
@@ -812,9 +802,10 @@ __global__ void __launch_bounds__(RB_CONS + 32, 2) k_point_pass_tma(PassArgs a) 
     for (int j = 0; j < RB_PPT; ++j) {
       const uint32_t v = val[j];
       const bool fast = !ATTR || ((fastm >> j) & 1u);
-      const uint32_t sv = v - 1u;
-      const bool common = (v != 0u) & ((sv & (RB_VALUE_LIST | 1u)) == 0u) & fast;
-      if (common) h.add_fast(sv, qv[j]);
+      // single interior owner: code = v & CODE_MASK (= 2*region + 1), hot slot in bits 18..29
+      const uint32_t sv = (v & RB_CODE_MASK) - 1u;
+      const bool common = (v != 0u) & ((v & RB_VALUE_LIST) == 0u) & ((sv & 1u) == 0u) & fast;
+      if (common) h.add(sv, v >> RB_HOT_SHIFT, w[j], qv[j], true);
       rarem |= (!common & (v != 0u)) ? (1u << j) : 0u;
     }
     // E. boundary owners, owner lists, out-of-window attributes
@@ -827,16 +818,12 @@ __global__ void __launch_bounds__(RB_CONS + 32, 2) k_point_pass_tma(PassArgs a) 
         }
       }
     }
-#if RB_LATE_RELEASE
-    __syncwarp();
-    if ((ct & 31) == 0) mbar_arrive(&empty_bar[st]);
-    if (++st == RB_NST) { st = 0; ph ^= 1u; }
-#endif
     if (ATTR && ++ep == 65536 / RB_TP) {  // fold the 16-bit fixed-point halves every 65536 points
       ep = 0;
       asm volatile("bar.sync 1, %0;" ::"r"(RB_CONS) : "memory");
-      for (int q = ct; q < R2; q += RB_CONS) {
-        acc[q] += ((long long)(int32_t)h3[3 * q + 2] << 16) + (long long)h3[3 * q + 1];
+      for (int q = ct; q < NB; q += RB_CONS) {
+        const long long f = ((long long)(int32_t)h3[3 * q + 2] << 16) + (long long)h3[3 * q + 1];
+        if (GH) a.part_acc[(size_t)blockIdx.x * NB + q] += f; else acc[q] += f;
         h3[3 * q + 1] = 0;
         h3[3 * q + 2] = 0;
       }
@@ -853,6 +840,21 @@ __global__ void __launch_bounds__(RB_CONS + 32, 2) k_point_pass_tma(PassArgs a) 
     }
   }
   asm volatile("bar.sync 1, %0;" ::"r"(RB_CONS) : "memory");
+  if (GH) {  // flush the hot bins into the global per-region outputs
+    const int Sx = ATTR ? *a.scale_exp : 0;
+    for (int q = ct; q < NB; q += RB_CONS) {
+      const uint32_t c = h3[ATTR ? 3 * q : q];
+      if (!c) continue;
+      const int32_t r = a.hot_region[q];
+      atomicAdd(&a.gcnt[2 * r], (unsigned long long)c);
+      if (ATTR) {
+        const long long f = a.part_acc[(size_t)blockIdx.x * NB + q] + ((long long)(int32_t)h3[3 * q + 2] << 16) +
+                            (long long)h3[3 * q + 1];
+        atomicAdd(&a.gsum[2 * r], ldexp((double)f, -Sx));
+      }
+    }
+    return;
+  }
   uint32_t* pc = a.part_cnt + (size_t)blockIdx.x * R2;
   long long* pa = a.part_acc + (size_t)blockIdx.x * R2;
   double* ps = a.part_sum + (size_t)blockIdx.x * R2;
@@ -867,7 +869,7 @@ __global__ void __launch_bounds__(RB_CONS + 32, 2) k_point_pass_tma(PassArgs a) 
 
 // binary scale of the SUM fixed point from a strided sample of the attribute
 __global__ void k_attr_scale(const float* attr, int64_t n, int* scale_exp) {
-  __shared__ float red[256];
+  __shared__ float red[1024];
   float m = 0.f;
   const int64_t stride = n / 4096 > 0 ? n / 4096 : 1;
   for (int64_t k = threadIdx.x; k < 4096 && k * stride < n; k += blockDim.x) {
@@ -892,20 +894,34 @@ __global__ void k_attr_scale(const float* attr, int64_t n, int* scale_exp) {
   }
 }
 
-// deterministic reduction of the fixed-point rows (fixed CTA order)
-__global__ void k_reduce_fixed(const uint32_t* part_cnt, const long long* part_acc, const double* part_sum, int nrows,
-                               int R2, bool attr, const int* scale_exp, int64_t* cnt_out, double* sum_out) {
-  const int S = attr ? *scale_exp : 0;
-  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < R2; q += gridDim.x * blockDim.x) {
-    uint64_t c = 0;
-    long long f = 0;
-    double s = 0.0;
-    for (int r = 0; r < nrows; ++r) {
+// deterministic reduction of the per-CTA rows: a block owns 32 consecutive
+// bins (lane = bin, coalesced row reads); its 32 warps stride over the rows
+// and are combined in fixed warp order.
+__global__ void __launch_bounds__(1024) k_reduce_fixed(const uint32_t* part_cnt, const long long* part_acc,
+                                                       const double* part_sum, int nrows, int R2, bool attr,
+                                                       const int* scale_exp, int64_t* cnt_out, double* sum_out) {
+  __shared__ unsigned long long sc[32][32];
+  __shared__ long long sa[32][32];
+  __shared__ double ss[32][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int q = blockIdx.x * 32 + lane;
+  unsigned long long c = 0;
+  long long f = 0;
+  double s = 0.0;
+  if (q < R2) {
+    for (int r = warp; r < nrows; r += 32) {
       c += part_cnt[(size_t)r * R2 + q];
       if (attr) { f += part_acc[(size_t)r * R2 + q]; s += part_sum[(size_t)r * R2 + q]; }
     }
+  }
+  sc[warp][lane] = c;
+  sa[warp][lane] = f;
+  ss[warp][lane] = s;
+  __syncthreads();
+  if (warp == 0 && q < R2) {
+    for (int w2 = 1; w2 < 32; ++w2) { c += sc[w2][lane]; f += sa[w2][lane]; s += ss[w2][lane]; }
     cnt_out[q] += (int64_t)c;
-    if (attr) sum_out[q] += ldexp((double)f, -S) + s;
+    if (attr) sum_out[q] += ldexp((double)f, -*scale_exp) + s;
   }
 }
 
@@ -955,7 +971,7 @@ static void pool_keep_warm() {
 
 // largest region count whose histogram (28 B per bin pair entry) fits the
 // 200 KB shared-memory budget of one CTA
-#define RB_SMEM_BUDGET (200 * 1024)
+#define RB_SMEM_BUDGET (226 * 1024)
 
 template <int XY, bool ATTR, bool VEC>
 static cudaError_t launch_smem(const PassArgs& a, size_t smem, cudaStream_t s, int* blocks_out) {
@@ -974,9 +990,11 @@ static cudaError_t launch_smem(const PassArgs& a, size_t smem, cudaStream_t s, i
   *blocks_out = cached_blocks;
   return cudaSuccess;
 }
-template <int XY, bool ATTR>
-static cudaError_t launch_tma(size_t smem, int* blocks_out) {
-  auto kern = k_point_pass_tma<XY, ATTR>;
+static int g_kernel_sel = -1;  // 0 = synchronous loads (fallback), 1 = TMA ring (default)
+
+template <int XY, bool ATTR, bool GH>
+static cudaError_t tma_blocks(size_t smem, int* blocks_out) {
+  auto kern = k_point_pass_tma<XY, ATTR, GH>;
   static int cached_blocks = -1;
   static size_t cached_smem = 0;
   if (cached_blocks < 0 || cached_smem != smem) {
@@ -992,11 +1010,27 @@ static cudaError_t launch_tma(size_t smem, int* blocks_out) {
   return cudaSuccess;
 }
 
+template <int XY, bool ATTR, bool GH>
+static cudaError_t tma_run(const PassArgs& a, int blocks, size_t smem, cudaStream_t s) {
+  k_point_pass_tma<XY, ATTR, GH><<<blocks, RB_CONS + 32, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
 template <int XY, bool ATTR, bool VEC>
 static cudaError_t run_smem(const PassArgs& a, int blocks, size_t smem, cudaStream_t s) {
   k_point_pass<XY, ATTR, VEC><<<blocks, 256, smem, s>>>(a);
   return cudaGetLastError();
 }
+
+#define RB_DISPATCH_TMA(FN, GHV, ...)                                                            \
+  (dtype == RB_XY_F64 ? (attr ? FN<0, true, GHV>(__VA_ARGS__) : FN<0, false, GHV>(__VA_ARGS__)) \
+                      : (attr ? FN<1, true, GHV>(__VA_ARGS__) : FN<1, false, GHV>(__VA_ARGS__)))
+#define RB_DISPATCH_SYNC(FN, ...)                                                                           \
+  (dtype == RB_XY_F64                                                                                       \
+       ? (attr ? (vec ? FN<0, true, true>(__VA_ARGS__) : FN<0, true, false>(__VA_ARGS__))                   \
+               : (vec ? FN<0, false, true>(__VA_ARGS__) : FN<0, false, false>(__VA_ARGS__)))                \
+       : (attr ? (vec ? FN<1, true, true>(__VA_ARGS__) : FN<1, true, false>(__VA_ARGS__))                   \
+               : (vec ? FN<1, false, true>(__VA_ARGS__) : FN<1, false, false>(__VA_ARGS__))))
 
 // flags: bit0 = zero the outputs first, bit1 = reset first_bad first
 int point_pass(const rb_approx* A, const void* xy, int32_t dtype, int64_t n, const float* attr, int64_t* cnt_out,
@@ -1005,6 +1039,10 @@ int point_pass(const rb_approx* A, const void* xy, int32_t dtype, int64_t n, con
     int dev = 0;
     RB_CUDA(cudaGetDevice(&dev));
     RB_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  if (g_kernel_sel < 0) {
+    const char* ks = getenv("RB_KERNEL");
+    g_kernel_sel = ks ? atoi(ks) : 1;
   }
   pool_keep_warm();
   const int R2 = 2 * A->n_regions;
@@ -1024,26 +1062,35 @@ int point_pass(const rb_approx* A, const void* xy, int32_t dtype, int64_t n, con
   a.gcnt = (unsigned long long*)cnt_out;
   a.gsum = sum_out;
   a.idx_base = idx_base;
-  const size_t per_bin = attr ? 28 : 4;
-  const bool smem_hist = (size_t)R2 * per_bin <= RB_SMEM_BUDGET;
-  const size_t smem = smem_hist ? (size_t)R2 * per_bin : 0;
-  const bool vec = ((uintptr_t)xy % 32 == 0) && (!attr || (uintptr_t)attr % (dtype == RB_XY_F64 ? 8 : 16) == 0);
+  a.hot_region = A->hot_region.as<int32_t>();
+  a.n_hot = A->n_hot;
   if (flags) {
     k_init_out<<<std::max(1, (R2 + 255) / 256), 256, 0, s>>>(cnt_out, sum_out, R2, flags, a.first_bad);
     RB_CUDA(cudaGetLastError());
     ++g_launches;
   }
   if (n == 0) return RB_OK;
+  const size_t pt_bytes = (dtype == RB_XY_F64 ? 16 : 8) + (attr ? 4 : 0);
+  const size_t ring = (size_t)RB_NST * RB_TP * pt_bytes;
+  const size_t summ_bytes = A->S >= 0 ? ((size_t)2 << (2 * A->S)) + 32 : 0;
+  const size_t all_bins = (size_t)R2 * (attr ? 28 : 4) + 16;
+  const size_t hot_bins = (((size_t)A->n_hot * (attr ? 12 : 4)) + 15) & ~(size_t)15;
+  const bool aligned = ((uintptr_t)xy % 16 == 0) && (!attr || (uintptr_t)attr % 16 == 0);
+  const bool vec = ((uintptr_t)xy % 32 == 0) && (!attr || (uintptr_t)attr % (dtype == RB_XY_F64 ? 8 : 16) == 0);
+  const bool use_tma = g_kernel_sel != 0 && aligned;
+  // histogram placement: every bin in shared memory when it fits next to the ring
+  const bool smem_hist = use_tma ? ring + all_bins + summ_bytes <= RB_SMEM_BUDGET
+                                 : (size_t)R2 * (attr ? 28 : 4) <= RB_SMEM_BUDGET;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  if (!smem_hist) {
-    int blocks = g_num_sms * 4;
+  auto tstart = [&]() -> int {
     if (g_timing) {
       RB_CUDA(cudaEventCreate(&ev0));
       RB_CUDA(cudaEventCreate(&ev1));
       RB_CUDA(cudaEventRecord(ev0, s));
     }
-    cudaError_t e = dtype == RB_XY_F64 ? launch_a<0, false>(a, vec, blocks, 0, s) : launch_a<1, false>(a, vec, blocks, 0, s);
-    if (e) return cuda_fail(e, "k_point_pass_global");
+    return RB_OK;
+  };
+  auto tstop = [&]() -> int {
     ++g_launches;
     if (g_timing) {
       RB_CUDA(cudaEventRecord(ev1, s));
@@ -1051,76 +1098,56 @@ int point_pass(const rb_approx* A, const void* xy, int32_t dtype, int64_t n, con
       g_events.emplace_back(ev0, ev1);
     }
     return RB_OK;
+  };
+  cudaError_t e = cudaSuccess;
+  if (!smem_hist && !use_tma) {  // fallback for misaligned inputs with large region sets
+    const int blocks = g_num_sms * 4;
+    if (tstart()) return RB_CUDA_ERROR;
+    e = dtype == RB_XY_F64 ? launch_a<0, false>(a, vec, blocks, 0, s) : launch_a<1, false>(a, vec, blocks, 0, s);
+    if (e) return cuda_fail(e, "k_point_pass_global");
+    return tstop();
   }
   int blocks = 0;
-  cudaError_t e;
-  const size_t summ_bytes = A->S >= 0 ? ((size_t)2 << (2 * A->S)) + 32 : 0;
-  static const bool no_tma = getenv("RB_NO_TMA") != nullptr;
-  const bool tma = !no_tma && ((uintptr_t)xy % 16 == 0) && (!attr || (uintptr_t)attr % 16 == 0) &&
-                   (size_t)RB_NST * RB_TP * ((dtype == RB_XY_F64 ? 16 : 8) + (attr ? 4 : 0)) + smem + summ_bytes <=
-                       RB_SMEM_BUDGET;
-#define RB_DISPATCH(FN, ...)                                                                          \
-  if (dtype == RB_XY_F64) {                                                                           \
-    if (attr) e = vec ? FN<0, true, true>(__VA_ARGS__) : FN<0, true, false>(__VA_ARGS__);             \
-    else e = vec ? FN<0, false, true>(__VA_ARGS__) : FN<0, false, false>(__VA_ARGS__);                \
-  } else {                                                                                            \
-    if (attr) e = vec ? FN<1, true, true>(__VA_ARGS__) : FN<1, true, false>(__VA_ARGS__);             \
-    else e = vec ? FN<1, false, true>(__VA_ARGS__) : FN<1, false, false>(__VA_ARGS__);                \
-  }
-  size_t tma_smem = 0;
-  if (tma) {
-    tma_smem = (size_t)RB_NST * RB_TP * ((dtype == RB_XY_F64 ? 16 : 8) + (attr ? 4 : 0)) + smem + summ_bytes;
-    e = dtype == RB_XY_F64 ? (attr ? launch_tma<0, true>(tma_smem, &blocks) : launch_tma<0, false>(tma_smem, &blocks))
-                           : (attr ? launch_tma<1, true>(tma_smem, &blocks) : launch_tma<1, false>(tma_smem, &blocks));
+  size_t smem = 0;
+  if (use_tma) {
+    smem = ring + (smem_hist ? all_bins : hot_bins) + summ_bytes;
+    e = smem_hist ? RB_DISPATCH_TMA(tma_blocks, false, smem, &blocks) : RB_DISPATCH_TMA(tma_blocks, true, smem, &blocks);
   } else {
-    RB_DISPATCH(launch_smem, a, smem, s, &blocks);
+    smem = (size_t)R2 * (attr ? 28 : 4);
+    e = RB_DISPATCH_SYNC(launch_smem, a, smem, s, &blocks);
   }
   if (e) return cuda_fail(e, "k_point_pass setup");
+  // scratch: per-CTA rows (smem mode: all bins; global mode: hot fixed-point accumulators) + scale
   void* scratch = nullptr;
-  const size_t rows = (size_t)blocks * R2;
-  RB_CUDA(cudaMallocAsync(&scratch, rows * (4 + 8 + 8) + 16, s));
+  const size_t rows = smem_hist ? (size_t)blocks * R2 : (size_t)blocks * std::max(A->n_hot, 1);
+  const size_t sbytes = smem_hist ? rows * (4 + 8 + 8) + 16 : rows * 8 + 16;
+  RB_CUDA(cudaMallocAsync(&scratch, sbytes, s));
   a.part_acc = (long long*)scratch;
-  a.part_sum = (double*)((char*)scratch + rows * 8);
-  a.part_cnt = (uint32_t*)((char*)scratch + rows * 16);
-  int* scale = (int*)((char*)scratch + rows * 20);
+  a.part_sum = smem_hist ? (double*)((char*)scratch + rows * 8) : nullptr;
+  a.part_cnt = smem_hist ? (uint32_t*)((char*)scratch + rows * 16) : nullptr;
+  int* scale = (int*)((char*)scratch + (smem_hist ? rows * 20 : rows * 8));
   a.scale_exp = scale;
   if (attr) {
-    k_attr_scale<<<1, 256, 0, s>>>(attr, n, scale);
+    k_attr_scale<<<1, 1024, 0, s>>>(attr, n, scale);
     RB_CUDA(cudaGetLastError());
     ++g_launches;
   }
-  if (g_timing) {
-    RB_CUDA(cudaEventCreate(&ev0));
-    RB_CUDA(cudaEventCreate(&ev1));
-    RB_CUDA(cudaEventRecord(ev0, s));
-  }
-  if (tma) {
-    if (dtype == RB_XY_F64) {
-      if (attr) k_point_pass_tma<0, true><<<blocks, RB_CONS + 32, tma_smem, s>>>(a);
-      else k_point_pass_tma<0, false><<<blocks, RB_CONS + 32, tma_smem, s>>>(a);
-    } else {
-      if (attr) k_point_pass_tma<1, true><<<blocks, RB_CONS + 32, tma_smem, s>>>(a);
-      else k_point_pass_tma<1, false><<<blocks, RB_CONS + 32, tma_smem, s>>>(a);
-    }
-    e = cudaGetLastError();
-  } else {
-    RB_DISPATCH(run_smem, a, blocks, smem, s);
-  }
-#undef RB_DISPATCH
+  if (tstart()) return RB_CUDA_ERROR;
+  if (use_tma) e = smem_hist ? RB_DISPATCH_TMA(tma_run, false, a, blocks, smem, s) : RB_DISPATCH_TMA(tma_run, true, a, blocks, smem, s);
+  else e = RB_DISPATCH_SYNC(run_smem, a, blocks, smem, s);
   if (e) return cuda_fail(e, "k_point_pass");
-  ++g_launches;
-  if (g_timing) {
-    RB_CUDA(cudaEventRecord(ev1, s));
-    std::lock_guard<std::mutex> lk(g_ev_mu);
-    g_events.emplace_back(ev0, ev1);
+  if (tstop()) return RB_CUDA_ERROR;
+  if (smem_hist) {
+    k_reduce_fixed<<<std::max(1, (R2 + 31) / 32), 1024, 0, s>>>(a.part_cnt, a.part_acc, a.part_sum, blocks, R2,
+                                                                attr != nullptr, scale, cnt_out, sum_out);
+    RB_CUDA(cudaGetLastError());
+    ++g_launches;
   }
-  k_reduce_fixed<<<std::max(1, (R2 + 255) / 256), 256, 0, s>>>(a.part_cnt, a.part_acc, a.part_sum, blocks, R2,
-                                                               attr != nullptr, scale, cnt_out, sum_out);
-  RB_CUDA(cudaGetLastError());
-  ++g_launches;
   RB_CUDA(cudaFreeAsync(scratch, s));
   return RB_OK;
 }
+#undef RB_DISPATCH_TMA
+#undef RB_DISPATCH_SYNC
 
 // act_lookup for a batch: owner value per point
 __global__ void k_lookup(IndexView V, double ox, double oy, double side, double inv_side, double lim, const void* xy,
@@ -1135,7 +1162,8 @@ __global__ void k_lookup(IndexView V, double ox, double oy, double side, double 
       out[i] = 0;
       continue;
     }
-    out[i] = index_lookup(V, (uint32_t)fx, (uint32_t)fy);
+    const uint32_t v = index_lookup(V, (uint32_t)fx, (uint32_t)fy);
+    out[i] = (v & RB_VALUE_LIST) ? v : (v & RB_CODE_MASK);  // public encoding (no hot annotation)
   }
 }
 

@@ -59,6 +59,37 @@ class ApproxIndex:
                                           C.byref(h)), "rasterize/act_build")
         self._h = h
         self._torch = torch
+        self._hot = None
+
+    # regions beyond what one CTA's shared memory holds are accumulated with
+    # global atomics; the most frequent owners are privatised ("hot" slots)
+    HOT_THRESHOLD = 1024
+
+    def set_hot(self, regions) -> None:
+        """rb_approx_set_hot: privatise these (dense) region indices in shared memory."""
+        torch = self._torch
+        r = torch.as_tensor(np.asarray(regions, dtype=np.int32)).contiguous()
+        N.check(self._lib.rb_approx_set_hot(self._h, r.data_ptr() if len(r) else None, int(len(r)),
+                                            N.stream_ptr()), "set_hot")
+        self._hot = r.numpy().copy()
+
+    def auto_hot(self, xy, k: int = N.MAX_HOT, sample: int = 1 << 20) -> np.ndarray:
+        """Pick the k most frequent single owners of a strided point sample."""
+        torch = self._torch
+        t, _ = self._xy(xy)
+        n = int(t.shape[0])
+        if n == 0:
+            self.set_hot([])
+            return self._hot
+        step = max(1, n // sample)
+        v = self.lookup(t[::step]).to(torch.int64) & 0xFFFFFFFF
+        single = (v != 0) & ((v & N.VALUE_LIST) == 0)
+        reg = (((v[single] & N.CODE_MASK) - 1) >> 1)
+        cnt = torch.bincount(reg, minlength=self.n_regions)
+        top = torch.argsort(cnt, descending=True)[:k]
+        top = top[cnt[top] > 0]
+        self.set_hot(top.sort().values.cpu().numpy())
+        return self._hot
 
     @classmethod
     def from_handle(cls, handle: C.c_void_p, grid: GridConfig, n_regions: int, layout: str, radix_width: int):
@@ -73,6 +104,7 @@ class ApproxIndex:
         self._lib = N.load()
         self._h = handle
         self._torch = N.require_cuda()
+        self._hot = None
         return self
 
     def __del__(self):
@@ -111,6 +143,8 @@ class ApproxIndex:
         torch = self._torch
         t, dt = self._xy(xy)
         n = int(t.shape[0])
+        if self._hot is None and self.n_regions > self.HOT_THRESHOLD:
+            self.auto_hot(t)
         a = None
         if attr is not None:
             a = attr if isinstance(attr, torch.Tensor) else torch.as_tensor(np.asarray(attr))
@@ -129,6 +163,9 @@ class ApproxIndex:
     def join_host(self, xy: np.ndarray, attr: np.ndarray | None = None):
         """rb_join_host: host (ideally pinned) buffers in, host results out."""
         xy = np.ascontiguousarray(xy) if isinstance(xy, np.ndarray) else xy
+        if self._hot is None and self.n_regions > self.HOT_THRESHOLD:
+            step = max(1, int(xy.shape[0]) // (1 << 20))
+            self.auto_hot(xy[::step])
         if isinstance(xy, np.ndarray):
             dt = N.XY_F64 if xy.dtype == np.float64 else N.XY_F32
             if xy.dtype not in (np.float64, np.float32):

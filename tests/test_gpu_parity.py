@@ -200,3 +200,22 @@ def test_join_host_matches_device(oracle_lib):
     cnt, sm = idx.join_host(w.xy, w.attrs["fare"])
     np.testing.assert_array_equal(cnt, r.cnt.cpu().numpy())
     np.testing.assert_allclose(sm, r.sum.cpu().numpy(), rtol=1e-12)
+
+
+def test_large_region_set_global_histogram(oracle_lib):
+    """3000 regions: the histogram no longer fits shared memory and the point
+    pass accumulates with global REDs -- same bit-exact COUNT."""
+    _gpu()
+    from paper_2010_12548_b200 import workloads as W
+
+    regions = W.voronoi_tiling(3000, 1.0, seed=4, verts=(10, 30))
+    grid = UNIT.with_level(13)
+    rng = np.random.default_rng(8)
+    xy = rng.random((1_000_001, 2))
+    xy32 = xy.astype(np.float32)
+    attr = rng.lognormal(2.5, 0.6, len(xy)).astype(np.float32)
+    for mode in (0, 1):
+        A, _ = oracle_approx(oracle_lib, regions, grid, mode)
+        idx = _prepared(regions, grid, mode, "trie")
+        _assert_join(idx, A, xy, attr)
+        _assert_join(idx, A, xy32, attr)
