@@ -215,11 +215,15 @@ def run_ours(a):
     peak, peak_src = peaks()
     k_ms = kms / max(timed, 1)
     achieved = n * C["bpp"] / (k_ms / 1e3) / 1e9
+    # ncu dram__bytes_read.sum + dram__bytes_write.sum of the point-pass kernel (one --set full
+    # capture, profiles/), scaled to this launch's point count; bytes per launch
     traffic = None
     prof = os.path.join(ROOT, "profiles", f"ncu_{a.config}_{layout}.json")
     if os.path.exists(prof):
         with open(prof) as f:
-            traffic = json.load(f).get("dram_bytes_per_launch")
+            pj = json.load(f)
+        if pj.get("dram_bytes_per_point"):
+            traffic = round(pj["dram_bytes_per_point"] * n)
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
             "kernel": "k_point_pass", "kernel_ms": round(k_ms, 4),

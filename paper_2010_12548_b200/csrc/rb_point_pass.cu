@@ -84,6 +84,8 @@ struct PassArgs {
   const int* scale_exp;
   const int32_t* hot_region;  // global mode: hot slot -> region
   int n_hot;
+  int hcopies;  // warp kernel: copies of the shared histogram (lane & (hcopies-1) picks one)
+  int hstride;  // warp kernel: words per histogram copy (== 1 mod 32: a bin's copies sit in distinct banks)
 };
 
 template <bool SMEM, bool ATTR>
@@ -313,8 +315,8 @@ __device__ __noinline__ void add_owners_i(IHist<ATTR> h, const uint32_t* __restr
 // predicated 32-bit read-only load: returns dflt without touching memory when !pred
 __device__ __forceinline__ uint32_t ldg_pred(const uint32_t* ptr, bool pred, uint32_t dflt) {
   uint32_t v;
-  asm volatile(
-      "{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n mov.u32 %0, %3;\n @p ld.global.nc.u32 %0, [%1];\n}\n"
+  // not volatile: a pure read of the immutable index, free to be scheduled with its neighbours
+  asm("{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n mov.u32 %0, %3;\n @p ld.global.nc.u32 %0, [%1];\n}\n"
       : "=r"(v)
       : "l"(ptr), "r"((uint32_t)pred), "r"(dflt));
   return v;
@@ -608,6 +610,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// warp-uniform wait: every lane polls and the warp leaves together (a per-lane
+// spin lets lanes leave at different times, and ITS keeps such a warp split)
+__device__ __forceinline__ uint32_t mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 100000;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok;
+}
+__device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t parity) {
+  while (!__all_sync(0xffffffffu, mbar_try(bar, parity))) {
+  }
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
@@ -867,6 +884,358 @@ __global__ void __launch_bounds__(RB_CONS + 32, RB_MINB_TMA) k_point_pass_tma(Pa
   }
 }
 
+// ---------------------------------------------------------------------------
+// Per-warp TMA rings (the production path for L <= 20 and a shared-memory
+// histogram).
+//
+// Every consumer warp is its own producer: lane 0 streams the warp's next
+// warp-tiles (PPT * 32 points of coordinates + attribute) into the warp's
+// private NST-stage ring with cp.async.bulk and a per-stage mbarrier.  A warp
+// refills a stage as soon as its own lanes have read it, so there is no
+// CTA-wide empty barrier and no producer warp; warps drift independently.
+//
+// Quantisation, bit-identical to floor(RN((v - o) / side)):
+// t = RN(RN(RN(v - o) * RN(1/side)) + 2^20).  For 0 <= q < 2^20 the high word
+// of t is 0x41300000 + floor(q) and the low word is q's fraction in units of
+// 2^-32; the product differs from the quotient by < 2^-31 (L <= 20), so unless
+// the fraction lies within 2^-29 of an integer floor(q) is exact.  Range:
+// (hx - 0x41300000) | (hy - 0x41300000) < 2^L covers q < 0, q >= 2^L, NaN and
+// infinities.  Points failing either test take the exact division.
+//
+// Lookup: level-S summary in shared memory (single owner of a whole summary
+// cell), else the L2-resident root table, then node levels (ACT descent,
+// SPEC.md:285-288).  Accumulation: one interior owner with
+// an in-window attribute -> three predicated u32 shared REDs (count, fixed-
+// point low 16 bits, signed high part); every other owner value on the
+// outlined path.
+// ---------------------------------------------------------------------------
+// shared-memory REDs on 32-bit shared addresses (the generic atomicAdd on a
+// pointer the compiler cannot prove shared becomes a generic ATOM)
+__device__ __forceinline__ void reds(uint32_t addr, uint32_t v) {
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
+// Rare path of the warp kernel: every owner of value v (boundary owner, owner
+// list) or an attribute outside the fixed-point window.  bins: shared address
+// of bin 0 (stride 12 bytes with an attribute, 4 without).
+template <bool ATTR>
+__device__ __forceinline__ void add_owners_w(uint32_t bins, double* slow, const uint32_t* __restrict__ pool, uint32_t v,
+                                          float w, int32_t qv, bool fast) {
+  uint32_t n = 1, e = v;
+  const uint32_t* Lp = nullptr;
+  if (v & RB_VALUE_LIST) {
+    Lp = pool + (v & RB_VALUE_PAYLOAD);
+    n = __ldg(Lp) & ~RB_POOL_COUNT_FLAG;
+  } else {
+    e = (v & RB_CODE_MASK) - 1u;  // (region << 1) | boundary
+  }
+  for (uint32_t i = 0; i < n; ++i) {
+    if (Lp) e = __ldg(Lp + 1 + i) & RB_CODE_MASK;
+    const uint32_t q = e & ~1u;
+    for (uint32_t b = q; b <= (q | (e & 1u)); ++b) {  // alpha bin, and beta when boundary
+      const uint32_t ad = bins + b * (ATTR ? 12u : 4u);
+      reds(ad, 1u);
+      if (ATTR) {
+        if (fast) { reds(ad + 4, (uint32_t)qv & 0xffffu); reds(ad + 8, (uint32_t)(qv >> 16)); }
+        else atomicAdd(&slow[b], (double)w);
+      }
+    }
+  }
+}
+
+template <int XY, bool ATTR, int NW, int PPT, int NST>
+__global__ void __launch_bounds__(NW * 32 + 32, 1) k_point_pass_ring(PassArgs a) {
+  constexpr int PB = XY == 0 ? 16 : 8;
+  constexpr int WT = PPT * 32;  // points per consumer warp per tile
+  constexpr int TP = NW * WT;   // points per CTA tile
+  constexpr uint32_t XYB = TP * PB, ATB = ATTR ? TP * 4 : 0, STAGE = XYB + ATB;
+  constexpr uint32_t BS = ATTR ? 12u : 4u;  // bytes per shared bin
+  // The histogram has C copies (lane & (C-1) picks one) so lanes of a warp that hit the same hot
+  // region add to different words in different banks: same-address REDs with distinct values
+  // serialise, and with clustered points a warp often holds several points of one region.
+  // Drain period: every consumer warp drains ALL bins of all copies after each FOLD of its tiles;
+  // between two drains of a copy-bin each warp adds <= FOLD * WT / C points to it, <= 63488 + 3 in
+  // total, so the low-half sums stay < 2^32 and the signed high-half sums within +-2^30 (|qv| < 2^30).
+  const int C = a.hcopies, P = a.hstride;
+  const int FOLD = C * (63488 / (NW * WT) > 0 ? 63488 / (NW * WT) : 1);
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ LevelDesc lv;
+  __shared__ __align__(8) uint64_t full[NST], empty[NST];
+  const int R2 = a.R2;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;  // warp NW is the producer
+  // layout: [NST stages][32 dummy bins][C histogram copies of P words][slow f64: R2][summary u16]
+  unsigned char* dummy = smem + (size_t)NST * STAGE;
+  uint32_t* h3 = (uint32_t*)(dummy + 32 * BS);
+  const size_t h3b = (((size_t)C * P * 4) + 15) & ~(size_t)15;
+  double* slow = (double*)((unsigned char*)h3 + h3b);
+  uint16_t* summ = (uint16_t*)((unsigned char*)h3 + h3b + (ATTR ? (size_t)R2 * 8 : 0));
+  long long* prow = a.part_acc + (size_t)blockIdx.x * R2;  // this CTA's fixed-point sums (global, REDG.64)
+  const int S = a.V.S >= 0 ? a.V.S : 0;
+  constexpr int NT = NW * 32 + 32;
+  for (int q = tid; q < C * P; q += NT) h3[q] = 0;
+  if (ATTR)
+    for (int q = tid; q < R2; q += NT) { slow[q] = 0.0; prow[q] = 0; }
+  if (a.V.S >= 0) {
+    const int nsum = 1 << (2 * S);
+    const uint4* src = (const uint4*)a.V.summary;
+    for (int q = tid; q < (nsum >> 3); q += NT) ((uint4*)summ)[q] = __ldg(src + q);
+    for (int q = (nsum & ~7) + tid; q < nsum; q += NT) summ[q] = a.V.summary[q];
+  } else if (tid == 0) {
+    summ[0] = 0xffffu;  // no summary: every point consults the index
+  }
+  if (tid < RB_MAX_NODE_LEVELS) {
+    lv.nodes[tid] = a.V.nodes[tid];
+    lv.ks[tid] = a.V.ks[tid];
+  }
+  if (tid == 0) {
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  const int64_t nmain = a.n & ~(int64_t)3;  // bulk copies move 16-byte granules
+  const int64_t ntiles = (nmain + TP - 1) / TP;
+  const int64_t G = gridDim.x;
+  if (warp == NW) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      uint64_t pol;
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+      int st = 0;
+      uint32_t ph = 0;
+      int64_t k = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += G, ++k) {
+        if (k >= NST) mbar_wait(&empty[st], ph ^ 1u);
+        const int64_t p0 = t * TP;
+        const uint32_t m = (uint32_t)(p0 + TP <= nmain ? TP : nmain - p0);
+        unsigned char* dst = smem + (size_t)st * STAGE;
+        mbar_expect_tx(&full[st], m * (PB + (ATTR ? 4 : 0)));
+        bulk_g2s(dst, (const char*)a.xy + p0 * PB, m * PB, &full[st], pol);
+        if (ATTR) bulk_g2s(dst + XYB, a.attr + p0, m * 4, &full[st], pol);
+        if (++st == NST) { st = 0; ph ^= 1u; }
+      }
+    }
+    return;
+  }
+  // -------------------------------------------------------------- consumers
+  float sc = 1.f;
+  uint32_t wminb = 0, wspan = 0;
+  if (ATTR) {
+    const int Sx = *a.scale_exp;
+    sc = __int_as_float((Sx + 127) << 23);
+    wminb = (uint32_t)((20 - Sx + 127) << 23);  // |w| in [2^(20-S), 2^(30-S)): exact 30-bit fixed point
+    wspan = (uint32_t)((30 - Sx + 127) << 23) - wminb;
+  }
+  const double ox = a.ox, oy = a.oy, inv_side = a.inv_side;
+  const uint32_t* __restrict__ root = a.V.root;
+  const uint32_t* __restrict__ pool = a.V.pool;
+  const uint32_t* __restrict__ nodes0 = a.V.nodes[0];
+  const int L = a.V.L, T0 = a.V.T0, s0 = L - T0, nlev = a.V.nlev, sS = L - S;
+  const uint32_t hibits = ~((1u << L) - 1u);
+  const uint32_t m0 = (1u << s0) - 1u;
+  const bool onelevel = nlev == 1 && a.V.ks[0] == s0;  // the node level is the leaf level (k = L - T0)
+  const uint32_t bins = smem_u32(h3) + (uint32_t)((lane & (C - 1)) * P) * 4u;  // this lane's copy
+  const uint32_t h3s = bins - BS;  // interior owner value v = 2*region + 1 -> bin 2*region at h3s + v * BS
+  const uint32_t dms = smem_u32(dummy) + lane * BS;
+  // ---- software pipeline over this CTA's tiles (k = 0, 1, ...); iteration k runs
+  //   C(k-2): accumulate the owner values nv[] loaded during iteration k-1
+  //   B(k-1): node levels of tile k-1 from its root values rv[] (loaded during iteration k-1) -> nv[]
+  //   A(k)  : tile k: ring -> quantise -> summary -> root loads -> rv[]
+  // Each load is consumed one iteration after it is issued, and a load's destination register is
+  // only read by the consuming stage (no register copy waits on a load in flight).
+  uint32_t rv[PPT], bx[PPT], by[PPT], nv[PPT];
+  float w1[PPT], w2[PPT];
+#pragma unroll
+  for (int j = 0; j < PPT; ++j) { rv[j] = bx[j] = by[j] = nv[j] = 0u; w1[j] = w2[j] = 0.f; }
+  int st = 0;
+  uint32_t ph = 0;
+  int dk = 0;
+  const int64_t K = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / G + 1 : 0;
+  for (int64_t k = 0; k < K + 2; ++k) {
+    // ------------------------------------------------------------ C(k-2)
+    if (k >= 2) {
+      bool anyrare = false;
+#pragma unroll
+      for (int j = 0; j < PPT; ++j) {
+        const uint32_t v = nv[j];
+        int32_t qv = 0;
+        bool fast = true;
+        if (ATTR) {
+          qv = __float2int_rn(w2[j] * sc);
+          fast = ((__float_as_uint(w2[j]) & 0x7fffffffu) - wminb) < wspan;
+        }
+        // interior single owner (odd code, no list) with an in-window attribute
+        const bool common = ((v & (RB_VALUE_LIST | 1u)) == 1u) & fast;
+        // unconditional REDs (a predicated RED becomes a branch): off-path points hit this lane's dummy bin
+        const uint32_t ad = common ? h3s + (v & RB_CODE_MASK) * BS : dms;
+        reds(ad, 1u);
+        if (ATTR) {
+          reds(ad + 4, (uint32_t)qv & 0xffffu);
+          reds(ad + 8, (uint32_t)(qv >> 16));
+        }
+        anyrare |= !common & (v != 0u);
+      }
+      if (__any_sync(0xffffffffu, anyrare)) {  // boundary owners, owner lists, out-of-window attributes
+#pragma unroll
+        for (int j = 0; j < PPT; ++j) {
+          const uint32_t v = nv[j];
+          const bool fast = !ATTR || (((__float_as_uint(w2[j]) & 0x7fffffffu) - wminb) < wspan);
+          const bool common = ((v & (RB_VALUE_LIST | 1u)) == 1u) & fast;
+          if (!common && v != 0u)
+            add_owners_w<ATTR>(bins, slow, pool, v, w2[j], ATTR ? __float2int_rn(w2[j] * sc) : 0, fast);
+        }
+      }
+      if (ATTR && ++dk == FOLD) {  // drain the 16-bit fixed-point halves into this CTA's global row
+        dk = 0;
+        __syncwarp();
+        for (int q = lane; q < R2; q += 32) {
+          long long f = 0;
+          for (int c = 0; c < C; ++c) {
+            const uint32_t lo = atomicExch(&h3[c * P + 3 * q + 1], 0u);
+            const uint32_t hi = atomicExch(&h3[c * P + 3 * q + 2], 0u);
+            f += ((long long)(int32_t)hi << 16) + (long long)lo;
+          }
+          if (f) atomicAdd((unsigned long long*)&prow[q], (unsigned long long)f);
+        }
+      }
+    }
+    // ------------------------------------------------------------ B(k-1)
+    if (k >= 1 && k <= K) {
+#pragma unroll
+      for (int j = 0; j < PPT; ++j) { nv[j] = rv[j]; w2[j] = w1[j]; }
+      uint32_t anyn = 0;
+#pragma unroll
+      for (int j = 0; j < PPT; ++j) anyn |= rv[j];
+      if (__any_sync(0xffffffffu, (int32_t)anyn < 0)) {  // RB_VALUE_NODE = bit 31
+        if (onelevel) {  // one node level = the leaf cells of a root cell, row-major
+#pragma unroll
+          for (int j = 0; j < PPT; ++j) {
+            const uint32_t slot = ((by[j] & m0) << s0) | (bx[j] & m0);
+            const uint32_t* np = nodes0 + (((size_t)(rv[j] & RB_VALUE_PAYLOAD) << (2 * s0)) + slot);
+            nv[j] = ldg_pred(np, (int32_t)rv[j] < 0, rv[j]);
+          }
+        } else {
+          int s = s0;
+#pragma unroll 1
+          for (int li = 0; li < nlev; ++li) {
+            const int kk = lv.ks[li];
+            const uint32_t* __restrict__ nodes = lv.nodes[li];
+            s -= kk;
+            const uint32_t msk = (1u << kk) - 1u;
+#pragma unroll
+            for (int j = 0; j < PPT; ++j) {
+              const uint32_t slot = (((by[j] >> s) & msk) << kk) | ((bx[j] >> s) & msk);
+              const uint32_t* np = nodes + (((size_t)(nv[j] & RB_VALUE_PAYLOAD) << (2 * kk)) + slot);
+              nv[j] = ldg_pred(np, (int32_t)nv[j] < 0, nv[j]);
+            }
+          }
+        }
+      }
+    }
+    // ------------------------------------------------------------ A(k)
+    if (k < K) {
+      const int64_t t = blockIdx.x + k * G;
+      mbar_wait_warp(&full[st], ph);
+      const unsigned char* tile = smem + (size_t)st * STAGE;
+      double x[PPT], y[PPT];
+#pragma unroll
+      for (int j = 0; j < PPT; ++j) {
+        const int pi = warp * WT + lane + 32 * j;
+        if (XY == 0) {
+          const double2 v2 = ((const double2*)tile)[pi];
+          x[j] = v2.x; y[j] = v2.y;
+        } else {
+          const float2 v2 = ((const float2*)tile)[pi];
+          x[j] = (double)v2.x; y[j] = (double)v2.y;
+        }
+        w1[j] = ATTR ? ((const float*)(tile + XYB))[pi] : 0.f;
+      }
+      // the stage's generic-proxy reads precede the async-proxy refill that the arrive enables
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+      if (++st == NST) { st = 0; ph ^= 1u; }
+      // quantise: t = RN((v - o) * RN(1/side) + 2^20) (one rounding); high word = 0x41300000 +
+      // floor(q) for 0 <= q < 2^20, low word = fraction * 2^32; |t - 2^20 - RN(d/side)| < 2^-31
+      bool anybad = false;
+#pragma unroll
+      for (int j = 0; j < PPT; ++j) {
+        const double tx = __fma_rn(__dsub_rn(x[j], ox), inv_side, 1048576.0);
+        const double ty = __fma_rn(__dsub_rn(y[j], oy), inv_side, 1048576.0);
+        bx[j] = (uint32_t)__double2hiint(tx) - 0x41300000u;
+        by[j] = (uint32_t)__double2hiint(ty) - 0x41300000u;
+        const uint32_t fx = (uint32_t)__double2loint(tx) + 8u, fy = (uint32_t)__double2loint(ty) + 8u;
+        anybad |= ((bx[j] | by[j]) & hibits) != 0u;  // q < 0, q >= 2^L, NaN, inf
+        anybad |= (fx < 16u) | (fy < 16u);             // within 2^-29 of a cell edge
+      }
+      const int64_t p0 = t * TP + warp * WT;  // this warp's slice of the tile
+      uint32_t killm = 0;
+      if (__any_sync(0xffffffffu, anybad) || p0 + WT > nmain) {  // rare: exact division, domain errors, partial tile
+        const int64_t mm = nmain - p0;
+        const int m = (int)(mm >= WT ? WT : (mm > 0 ? mm : 0));
+#pragma unroll
+        for (int j = 0; j < PPT; ++j) {
+          const double tx = __fma_rn(__dsub_rn(x[j], ox), inv_side, 1048576.0);
+          const double ty = __fma_rn(__dsub_rn(y[j], oy), inv_side, 1048576.0);
+          const uint32_t fx = (uint32_t)__double2loint(tx) + 8u, fy = (uint32_t)__double2loint(ty) + 8u;
+          const bool bad = (((bx[j] | by[j]) & hibits) != 0u) | (fx < 16u) | (fy < 16u);
+          if (lane + 32 * j >= m) {
+            bx[j] = 0; by[j] = 0; killm |= 1u << j;
+          } else if (bad) {
+            const uint64_t qq =
+                quantize_exact(a.xy, p0 + lane + 32 * j, XY, ox, oy, a.side, a.lim, a.first_bad, a.idx_base);
+            if (qq != ~0ull) { bx[j] = (uint32_t)qq; by[j] = (uint32_t)(qq >> 32); }
+            else { bx[j] = 0; by[j] = 0; killm |= 1u << j; }
+          }
+        }
+      }
+      // summary (shared memory), else the radix table (L2)
+      uint32_t sv[PPT];
+#pragma unroll
+      for (int j = 0; j < PPT; ++j) sv[j] = summ[((by[j] >> sS) << S) | (bx[j] >> sS)];
+      if (killm) {
+#pragma unroll
+        for (int j = 0; j < PPT; ++j)
+          if (killm & (1u << j)) sv[j] = 0u;  // no owner, no lookup
+      }
+#pragma unroll
+      for (int j = 0; j < PPT; ++j) {
+        const uint32_t* rp = root + (((by[j] >> s0) << T0) | (bx[j] >> s0));
+        rv[j] = ldg_pred(rp, sv[j] == 0xffffu, sv[j]);
+      }
+    }
+  }
+  // up to 3 trailing points (n not a multiple of 4): CTA 0, float64 path
+  if (blockIdx.x == 0 && tid < (int)(a.n - nmain)) {
+    const int64_t i = nmain + tid;
+    const uint64_t qq = quantize_exact(a.xy, i, XY, ox, oy, a.side, a.lim, a.first_bad, a.idx_base);
+    if (qq != ~0ull) {
+      const uint32_t v = index_lookup(a.V, (uint32_t)qq, (uint32_t)(qq >> 32));
+      if (v != 0u) add_owners_w<ATTR>(bins, slow, pool, v, ATTR ? a.attr[i] : 0.f, 0, false);
+    }
+  }
+  asm volatile("bar.sync 1, %0;" ::"r"(NW * 32) : "memory");  // consumers only (the producer has left)
+  uint32_t* pc = a.part_cnt + (size_t)blockIdx.x * R2;
+  double* ps = a.part_sum + (size_t)blockIdx.x * R2;
+  for (int q = tid; q < R2; q += NW * 32) {
+    uint32_t cnt = 0;
+    long long f = 0;
+    for (int c = 0; c < C; ++c) {
+      const uint32_t* b = h3 + c * P + (ATTR ? 3 * q : q);
+      cnt += b[0];
+      if (ATTR) f += ((long long)(int32_t)b[2] << 16) + (long long)b[1];
+    }
+    pc[q] = cnt;
+    if (ATTR) {
+      if (f) atomicAdd((unsigned long long*)&prow[q], (unsigned long long)f);  // after this CTA's drains
+      ps[q] = slow[q];
+    }
+  }
+}
+
 // binary scale of the SUM fixed point from a strided sample of the attribute
 __global__ void k_attr_scale(const float* attr, int64_t n, int* scale_exp) {
   __shared__ float red[1024];
@@ -1022,7 +1391,41 @@ static cudaError_t run_smem(const PassArgs& a, int blocks, size_t smem, cudaStre
   return cudaGetLastError();
 }
 
-#define RB_DISPATCH_TMA(FN, GHV, ...)                                                            \
+// per-warp-ring kernel configurations (consumer warps, points per lane, stages)
+struct WarpCfg { int nw, ppt, nst; };
+static const WarpCfg kWarpCfgs[] = {{16, 4, 4}, {16, 4, 3}, {8, 4, 6}, {16, 2, 6}};
+
+template <int XY, bool ATTR, int NW, int PPT, int NST>
+static cudaError_t warp_run(const PassArgs& a, size_t smem, cudaStream_t s, int* blocks, bool launch) {
+  auto kern = k_point_pass_ring<XY, ATTR, NW, PPT, NST>;
+  static int cached_blocks = -1;
+  static size_t cached_smem = 0;
+  if (cached_blocks < 0 || cached_smem != smem) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, RB_SMEM_BUDGET);
+    if (e) return e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NW * 32 + 32, smem);
+    if (e) return e;
+    cached_blocks = per_sm * g_num_sms;
+    cached_smem = smem;
+  }
+  *blocks = cached_blocks;
+  if (!launch || cached_blocks <= 0) return cudaSuccess;
+  kern<<<cached_blocks, NW * 32 + 32, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+template <int XY, bool ATTR>
+static cudaError_t warp_dispatch(int ci, const PassArgs& a, size_t smem, cudaStream_t s, int* blocks, bool launch) {
+  switch (ci) {
+    case 0: return warp_run<XY, ATTR, 16, 4, 4>(a, smem, s, blocks, launch);
+    case 1: return warp_run<XY, ATTR, 16, 4, 3>(a, smem, s, blocks, launch);
+    case 2: return warp_run<XY, ATTR, 8, 4, 6>(a, smem, s, blocks, launch);
+    default: return warp_run<XY, ATTR, 16, 2, 6>(a, smem, s, blocks, launch);
+  }
+}
+
+#define RB_DISPATCH_TMA(FN, GHV, ...)                                                          \
   (dtype == RB_XY_F64 ? (attr ? FN<0, true, GHV>(__VA_ARGS__) : FN<0, false, GHV>(__VA_ARGS__)) \
                       : (attr ? FN<1, true, GHV>(__VA_ARGS__) : FN<1, false, GHV>(__VA_ARGS__)))
 #define RB_DISPATCH_SYNC(FN, ...)                                                                           \
@@ -1109,6 +1512,73 @@ int point_pass(const rb_approx* A, const void* xy, int32_t dtype, int64_t n, con
   }
   int blocks = 0;
   size_t smem = 0;
+  // per-warp rings: shared-memory histogram, L <= 20 (the 2^20 quantisation window)
+  int wci = -1;
+  if (use_tma && smem_hist && L <= 20 && g_kernel_sel != 3) {
+    static int env_ci = -2;
+    if (env_ci == -2) {
+      const char* e = getenv("RB_WARP_CFG");
+      env_ci = e ? atoi(e) : -1;
+    }
+    static int env_copies = -2;
+    if (env_copies == -2) {
+      const char* e = getenv("RB_HIST_COPIES");
+      env_copies = e ? atoi(e) : -1;
+    }
+    const size_t summ_w = A->S >= 0 ? ((size_t)2 << (2 * A->S)) : 16;
+    const int ncfg = (int)(sizeof(kWarpCfgs) / sizeof(kWarpCfgs[0]));
+    // histogram copies: up to 8 with an attribute (distinct-value REDs to one word serialise;
+    // same-address count increments are aggregated by the hardware), 1 for COUNT
+    for (int c = 0; c < ncfg && wci < 0; ++c) {
+      if (env_ci >= 0 && c != env_ci) continue;
+      const WarpCfg& W = kWarpCfgs[c];
+      const int wpb = attr ? 3 : 1;
+      const int P = R2 * wpb + (int)((33 - (R2 * wpb) % 32) % 32);  // P % 32 == 1
+      for (int C = attr ? 8 : 1; C >= 1; C >>= 1) {
+        if (env_copies > 0 && C > env_copies) continue;
+        const size_t bins_w = 32 * (attr ? 12 : 4) + ((((size_t)C * P * 4) + 15) & ~(size_t)15) +
+                              (attr ? (size_t)R2 * 8 : 0);
+        const size_t need = (size_t)W.nw * W.nst * W.ppt * 32 * pt_bytes + bins_w + summ_w;
+        if (need <= RB_SMEM_BUDGET - 1024) { wci = c; smem = need; a.hcopies = C; a.hstride = P; break; }
+      }
+    }
+    if (wci >= 0) {
+      e = dtype == RB_XY_F64 ? (attr ? warp_dispatch<0, true>(wci, a, smem, s, &blocks, false)
+                                     : warp_dispatch<0, false>(wci, a, smem, s, &blocks, false))
+                             : (attr ? warp_dispatch<1, true>(wci, a, smem, s, &blocks, false)
+                                     : warp_dispatch<1, false>(wci, a, smem, s, &blocks, false));
+      if (e) return cuda_fail(e, "k_point_pass_ring setup");
+      if (blocks <= 0) wci = -1;
+    }
+  }
+  if (wci >= 0) {
+    void* scratch = nullptr;
+    const size_t rows = (size_t)blocks * R2;
+    RB_CUDA(cudaMallocAsync(&scratch, rows * 20 + 16, s));
+    a.part_acc = (long long*)scratch;
+    a.part_sum = (double*)((char*)scratch + rows * 8);
+    a.part_cnt = (uint32_t*)((char*)scratch + rows * 16);
+    int* scale = (int*)((char*)scratch + rows * 20);
+    a.scale_exp = scale;
+    if (attr) {
+      k_attr_scale<<<1, 1024, 0, s>>>(attr, n, scale);
+      RB_CUDA(cudaGetLastError());
+      ++g_launches;
+    }
+    if (tstart()) return RB_CUDA_ERROR;
+    e = dtype == RB_XY_F64 ? (attr ? warp_dispatch<0, true>(wci, a, smem, s, &blocks, true)
+                                   : warp_dispatch<0, false>(wci, a, smem, s, &blocks, true))
+                           : (attr ? warp_dispatch<1, true>(wci, a, smem, s, &blocks, true)
+                                   : warp_dispatch<1, false>(wci, a, smem, s, &blocks, true));
+    if (e) return cuda_fail(e, "k_point_pass_ring");
+    if (tstop()) return RB_CUDA_ERROR;
+    k_reduce_fixed<<<std::max(1, (R2 + 31) / 32), 1024, 0, s>>>(a.part_cnt, a.part_acc, a.part_sum, blocks, R2,
+                                                                attr != nullptr, scale, cnt_out, sum_out);
+    RB_CUDA(cudaGetLastError());
+    ++g_launches;
+    RB_CUDA(cudaFreeAsync(scratch, s));
+    return RB_OK;
+  }
   if (use_tma) {
     smem = ring + (smem_hist ? all_bins : hot_bins) + summ_bytes;
     e = smem_hist ? RB_DISPATCH_TMA(tma_blocks, false, smem, &blocks) : RB_DISPATCH_TMA(tma_blocks, true, smem, &blocks);

@@ -1,0 +1,52 @@
+// Shared-memory atomic throughput on B200 for the point-pass histogram:
+// lanes add to random bins of a 260-region (520-bin) histogram laid out with
+// stride 3 words (count, fixed-point low, fixed-point high).  Reports lane-ops
+// per SM-cycle for 1, 2 and 3 atomics per point and for warps/SM 8..32.
+#include <cstdio>
+#include <cstdint>
+__device__ __forceinline__ uint32_t xs(uint32_t& s) { s ^= s << 13; s ^= s >> 17; s ^= s << 5; return s; }
+template <int NA>
+__global__ void k(unsigned* out, int iters, uint32_t nb) {
+  extern __shared__ unsigned h[];
+  for (uint32_t i = threadIdx.x; i < nb * 3; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  uint32_t s = 0x9e3779b9u * (blockIdx.x * blockDim.x + threadIdx.x + 1);
+  uint32_t base = (uint32_t)__cvta_generic_to_shared(h);
+  for (int it = 0; it < iters; ++it) {
+    uint32_t b = (xs(s) & 0xffff) % nb;
+    uint32_t a = base + b * 12;
+    asm volatile("red.shared.add.u32 [%0], 1;" :: "r"(a));
+    if (NA >= 2) asm volatile("red.shared.add.u32 [%0+4], %1;" :: "r"(a), "r"(s & 0xffff));
+    if (NA >= 3) asm volatile("red.shared.add.u32 [%0+8], %1;" :: "r"(a), "r"(s >> 16));
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) if (h[i] == 0xdeadbeef) out[0] = 1;
+}
+// same loop without atomics (to subtract the RNG/loop cost)
+__global__ void k0(unsigned* out, int iters, uint32_t nb) {
+  uint32_t s = 0x9e3779b9u * (blockIdx.x * blockDim.x + threadIdx.x + 1), acc = 0;
+  for (int it = 0; it < iters; ++it) { uint32_t b = (xs(s) & 0xffff) % nb; acc += b * 12; }
+  if (acc == 0xdeadbeef) out[0] = acc;
+}
+int main() {
+  int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  int clk; cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+  unsigned* d; cudaMalloc(&d, 16);
+  cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+  const int iters = 4000;
+  for (uint32_t nb : {520u, 80000u / 12u * 2u}) for (int wps : {8, 16, 32}) for (int na = 0; na <= 3; ++na) {
+    int threads = wps * 32;
+    size_t smem = nb * 12;
+    void (*kern)(unsigned*, int, uint32_t) = na == 0 ? k0 : na == 1 ? k<1> : na == 2 ? k<2> : k<3>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    kern<<<sms, threads, na ? smem : 0>>>(d, iters, nb);
+    cudaEventRecord(a);
+    kern<<<sms, threads, na ? smem : 0>>>(d, iters, nb);
+    cudaEventRecord(b); cudaEventSynchronize(b);
+    float ms; cudaEventElapsedTime(&ms, a, b);
+    double lanes = (double)sms * threads * iters;
+    printf("{\"bins\":%u,\"warps_per_sm\":%d,\"atomics_per_pt\":%d,\"ms\":%.3f,\"pts_per_sm_clk\":%.3f,\"err\":\"%s\"}\n", nb, wps, na, ms,
+           lanes / (ms * 1e-3) / sms / (clk * 1e3), cudaGetErrorString(cudaGetLastError()));
+  }
+  return 0;
+}

@@ -63,7 +63,16 @@ print("-- top stalled instructions")
 for d in sorted(data, key=lambda d: -float(d[key] or 0))[:12]:
     print(f"  {float(d[key]) / S * 100:5.1f}%  {d['Source'][:90]}")
 if out_json:
-    dr = float(rawd.get("dram__bytes_read.sum", 0) or 0) + float(rawd.get("dram__bytes_write.sum", 0) or 0)
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+
+    def nbytes(k):  # ncu prints each metric in its own unit (e.g. Gbyte for reads, Mbyte for writes)
+        if k not in rawd:
+            return 0.0
+        return float(str(rawd[k]).replace(",", "") or 0) * scale.get(ru[rh.index(k)], 1.0)
+
+    dr = nbytes("dram__bytes_read.sum") + nbytes("dram__bytes_write.sum")
     with open(out_json, "w") as f:
         json.dump({"report": rep, "metrics": {k: v for k, (v, u) in summary.items()},
-                   "dram_bytes_per_launch": dr, "stalls": {k: v / T for k, v in tot.items()}}, f, indent=1)
+                   "dram_bytes_per_launch": dr, "points": npts,
+                   "dram_bytes_per_point": dr / npts if npts else None,
+                   "stalls": {k: v / T for k, v in tot.items()}}, f, indent=1)
