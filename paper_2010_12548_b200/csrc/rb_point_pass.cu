@@ -86,6 +86,7 @@ struct PassArgs {
   int n_hot;
   int hcopies;  // warp kernel: copies of the shared histogram (lane & (hcopies-1) picks one)
   int hstride;  // warp kernel: words per histogram copy (== 1 mod 32: a bin's copies sit in distinct banks)
+  int ablate;   // timing experiments only (RB_ABLATE): 1 skip rare path, 2 skip node level, 4 skip root
 };
 
 template <bool SMEM, bool ATTR>
@@ -957,14 +958,17 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) k_point_pass_ring(PassArgs a)
   // between two drains of a copy-bin each warp adds <= FOLD * WT / C points to it, <= 63488 + 3 in
   // total, so the low-half sums stay < 2^32 and the signed high-half sums within +-2^30 (|qv| < 2^30).
   const int C = a.hcopies, P = a.hstride;
-  const int FOLD = C * (63488 / (NW * WT) > 0 ? 63488 / (NW * WT) : 1);
+  // (62000 leaves room for the <= 63 points a warp's rare queue carries across a drain)
+  const int FOLD = C * (62000 / (NW * WT) > 0 ? 62000 / (NW * WT) : 1);
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ LevelDesc lv;
   __shared__ __align__(8) uint64_t full[NST], empty[NST];
   const int R2 = a.R2;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;  // warp NW is the producer
-  // layout: [NST stages][32 dummy bins][C histogram copies of P words][slow f64: R2][summary u16]
-  unsigned char* dummy = smem + (size_t)NST * STAGE;
+  // layout: [NST stages][per-warp rare queues: NW x 64 x 8 B][32 dummy bins][C histogram copies of
+  // P words][slow f64: R2][summary u16]
+  uint2* rq = (uint2*)(smem + (size_t)NST * STAGE) + (size_t)(warp < NW ? warp : 0) * 64;
+  unsigned char* dummy = smem + (size_t)NST * STAGE + NW * 64 * 8;
   uint32_t* h3 = (uint32_t*)(dummy + 32 * BS);
   const size_t h3b = (((size_t)C * P * 4) + 15) & ~(size_t)15;
   double* slow = (double*)((unsigned char*)h3 + h3b);
@@ -1046,6 +1050,16 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) k_point_pass_ring(PassArgs a)
   //   A(k)  : tile k: ring -> quantise -> summary -> root loads -> rv[]
   // Each load is consumed one iteration after it is issued, and a load's destination register is
   // only read by the consuming stage (no register copy waits on a load in flight).
+  int qh = 0, qn = 0;  // this warp's rare queue: head, count (warp-uniform)
+  auto rare_flush = [&](int nitems) {
+    if (lane < nitems) {
+      const uint2 it = rq[(qh + lane) & 63];
+      const float ww = __uint_as_float(it.y);
+      const bool fast = !ATTR || (((it.y & 0x7fffffffu) - wminb) < wspan);
+      add_owners_w<ATTR>(bins, slow, pool, it.x, ww, ATTR ? __float2int_rn(ww * sc) : 0, fast);
+    }
+    __syncwarp();
+  };
   uint32_t rv[PPT], bx[PPT], by[PPT], nv[PPT];
   float w1[PPT], w2[PPT];
 #pragma unroll
@@ -1078,14 +1092,25 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) k_point_pass_ring(PassArgs a)
         }
         anyrare |= !common & (v != 0u);
       }
-      if (__any_sync(0xffffffffu, anyrare)) {  // boundary owners, owner lists, out-of-window attributes
+      // boundary owners, owner lists, out-of-window attributes: queue them per warp and process
+      // 32 at a time, one per lane (divergent one-lane processing cost a quarter of the pass)
+      if (!(a.ablate & 1) && __any_sync(0xffffffffu, anyrare)) {
 #pragma unroll
         for (int j = 0; j < PPT; ++j) {
           const uint32_t v = nv[j];
           const bool fast = !ATTR || (((__float_as_uint(w2[j]) & 0x7fffffffu) - wminb) < wspan);
-          const bool common = ((v & (RB_VALUE_LIST | 1u)) == 1u) & fast;
-          if (!common && v != 0u)
-            add_owners_w<ATTR>(bins, slow, pool, v, w2[j], ATTR ? __float2int_rn(w2[j] * sc) : 0, fast);
+          const bool rare = !(((v & (RB_VALUE_LIST | 1u)) == 1u) & fast) & (v != 0u);
+          const uint32_t mk = __ballot_sync(0xffffffffu, rare);
+          if (mk) {
+            if (rare) rq[(qh + qn + __popc(mk & ((1u << lane) - 1u))) & 63] = make_uint2(v, __float_as_uint(w2[j]));
+            qn += __popc(mk);
+            if (qn >= 32) {
+              __syncwarp();
+              rare_flush(32);
+              qh = (qh + 32) & 63;
+              qn -= 32;
+            }
+          }
         }
       }
       if (ATTR && ++dk == FOLD) {  // drain the 16-bit fixed-point halves into this CTA's global row
@@ -1109,7 +1134,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) k_point_pass_ring(PassArgs a)
       uint32_t anyn = 0;
 #pragma unroll
       for (int j = 0; j < PPT; ++j) anyn |= rv[j];
-      if (__any_sync(0xffffffffu, (int32_t)anyn < 0)) {  // RB_VALUE_NODE = bit 31
+      if (!(a.ablate & 2) && __any_sync(0xffffffffu, (int32_t)anyn < 0)) {  // RB_VALUE_NODE = bit 31
         if (onelevel) {  // one node level = the leaf cells of a root cell, row-major
 #pragma unroll
           for (int j = 0; j < PPT; ++j) {
@@ -1204,10 +1229,12 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) k_point_pass_ring(PassArgs a)
 #pragma unroll
       for (int j = 0; j < PPT; ++j) {
         const uint32_t* rp = root + (((by[j] >> s0) << T0) | (bx[j] >> s0));
-        rv[j] = ldg_pred(rp, sv[j] == 0xffffu, sv[j]);
+        rv[j] = ldg_pred(rp, sv[j] == 0xffffu && !(a.ablate & 4), sv[j]);
       }
     }
   }
+  __syncwarp();
+  if (qn) rare_flush(qn);
   // up to 3 trailing points (n not a multiple of 4): CTA 0, float64 path
   if (blockIdx.x == 0 && tid < (int)(a.n - nmain)) {
     const int64_t i = nmain + tid;
@@ -1536,7 +1563,7 @@ int point_pass(const rb_approx* A, const void* xy, int32_t dtype, int64_t n, con
       const int P = R2 * wpb + (int)((33 - (R2 * wpb) % 32) % 32);  // P % 32 == 1
       for (int C = attr ? 8 : 1; C >= 1; C >>= 1) {
         if (env_copies > 0 && C > env_copies) continue;
-        const size_t bins_w = 32 * (attr ? 12 : 4) + ((((size_t)C * P * 4) + 15) & ~(size_t)15) +
+        const size_t bins_w = (size_t)W.nw * 512 + 32 * (attr ? 12 : 4) + ((((size_t)C * P * 4) + 15) & ~(size_t)15) +
                               (attr ? (size_t)R2 * 8 : 0);
         const size_t need = (size_t)W.nw * W.nst * W.ppt * 32 * pt_bytes + bins_w + summ_w;
         if (need <= RB_SMEM_BUDGET - 1024) { wci = c; smem = need; a.hcopies = C; a.hstride = P; break; }
@@ -1552,6 +1579,12 @@ int point_pass(const rb_approx* A, const void* xy, int32_t dtype, int64_t n, con
     }
   }
   if (wci >= 0) {
+    static int env_ablate = -1;
+    if (env_ablate < 0) {
+      const char* e = getenv("RB_ABLATE");
+      env_ablate = e ? atoi(e) : 0;
+    }
+    a.ablate = env_ablate;
     void* scratch = nullptr;
     const size_t rows = (size_t)blocks * R2;
     RB_CUDA(cudaMallocAsync(&scratch, rows * 20 + 16, s));
