@@ -911,7 +911,7 @@ static int index_impl(int L, int64_t total_cells, const int32_t* cp_in, const ui
   // summary table for the shared-memory fast path (owner values must fit u16)
   {
     int Smax = RB_SUMMARY_DEFAULT;
-    if (const char* e = getenv("RB_SUMMARY_LEVEL")) Smax = atoi(e);
+    if (const char* e = getenv("RB_SUMMARY_LEVEL")) Smax = std::min(atoi(e), 8);  // <= 128 KB of shared memory
     A->S = -1;
     if (Smax >= 0 && 2 * (int64_t)A->n_regions + 1 < 0xffff) {
       const int S = std::min(Smax, T0);

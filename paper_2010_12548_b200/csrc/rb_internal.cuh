@@ -187,6 +187,7 @@ struct IndexView {
   int L, T0;
   const uint16_t* summary;  // level-S table of single owner values (0xffff = consult the index)
   int S;
+  int64_t nodes0_len;  // entries of the first node level (32-bit offsets when < 2^32)
 };
 
 // Owner value of leaf (ix, iy): descend the radix table (ACT lookup,
@@ -240,6 +241,7 @@ struct rb_approx {
     v.T0 = T0;
     v.summary = summary.as<uint16_t>();
     v.S = S;
+    v.nodes0_len = v.nlev > 0 ? (int64_t)(node_bufs[0].bytes / 4) : 0;
     return v;
   }
 };

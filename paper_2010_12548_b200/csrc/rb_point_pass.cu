@@ -945,7 +945,7 @@ __device__ __forceinline__ void add_owners_w(uint32_t bins, double* slow, const 
 }
 
 template <int XY, bool ATTR, int NW, int PPT, int NST>
-__global__ void __launch_bounds__(NW * 32 + 32, 1) k_point_pass_ring(PassArgs a) {
+__global__ void __launch_bounds__(NW * 32 + 32, NW <= 8 ? 2 : 1) k_point_pass_ring(PassArgs a) {
   constexpr int PB = XY == 0 ? 16 : 8;
   constexpr int WT = PPT * 32;  // points per consumer warp per tile
   constexpr int TP = NW * WT;   // points per CTA tile
@@ -1040,7 +1040,8 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) k_point_pass_ring(PassArgs a)
   const int L = a.V.L, T0 = a.V.T0, s0 = L - T0, nlev = a.V.nlev, sS = L - S;
   const uint32_t hibits = ~((1u << L) - 1u);
   const uint32_t m0 = (1u << s0) - 1u;
-  const bool onelevel = nlev == 1 && a.V.ks[0] == s0;  // the node level is the leaf level (k = L - T0)
+  // the single node level is the leaf level (k = L - T0), addressable with 32-bit offsets
+  const bool onelevel = nlev == 1 && a.V.ks[0] == s0 && a.V.nodes0_len < (int64_t(1) << 32);
   const uint32_t bins = smem_u32(h3) + (uint32_t)((lane & (C - 1)) * P) * 4u;  // this lane's copy
   const uint32_t h3s = bins - BS;  // interior owner value v = 2*region + 1 -> bin 2*region at h3s + v * BS
   const uint32_t dms = smem_u32(dummy) + lane * BS;
@@ -1130,19 +1131,20 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) k_point_pass_ring(PassArgs a)
     // ------------------------------------------------------------ B(k-1)
     if (k >= 1 && k <= K) {
 #pragma unroll
-      for (int j = 0; j < PPT; ++j) { nv[j] = rv[j]; w2[j] = w1[j]; }
+      for (int j = 0; j < PPT; ++j) w2[j] = w1[j];
       uint32_t anyn = 0;
 #pragma unroll
       for (int j = 0; j < PPT; ++j) anyn |= rv[j];
       if (!(a.ablate & 2) && __any_sync(0xffffffffu, (int32_t)anyn < 0)) {  // RB_VALUE_NODE = bit 31
-        if (onelevel) {  // one node level = the leaf cells of a root cell, row-major
+        if (onelevel) {  // one node level = the leaf cells of a root cell, row-major (32-bit offsets)
 #pragma unroll
           for (int j = 0; j < PPT; ++j) {
-            const uint32_t slot = ((by[j] & m0) << s0) | (bx[j] & m0);
-            const uint32_t* np = nodes0 + (((size_t)(rv[j] & RB_VALUE_PAYLOAD) << (2 * s0)) + slot);
-            nv[j] = ldg_pred(np, (int32_t)rv[j] < 0, rv[j]);
+            const uint32_t off = ((rv[j] & RB_VALUE_PAYLOAD) << (2 * s0)) | ((by[j] & m0) << s0) | (bx[j] & m0);
+            nv[j] = ldg_pred(nodes0 + off, (int32_t)rv[j] < 0, rv[j]);
           }
         } else {
+#pragma unroll
+          for (int j = 0; j < PPT; ++j) nv[j] = rv[j];
           int s = s0;
 #pragma unroll 1
           for (int li = 0; li < nlev; ++li) {
@@ -1158,6 +1160,9 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) k_point_pass_ring(PassArgs a)
             }
           }
         }
+      } else {
+#pragma unroll
+        for (int j = 0; j < PPT; ++j) nv[j] = rv[j];
       }
     }
     // ------------------------------------------------------------ A(k)
@@ -1420,7 +1425,7 @@ static cudaError_t run_smem(const PassArgs& a, int blocks, size_t smem, cudaStre
 
 // per-warp-ring kernel configurations (consumer warps, points per lane, stages)
 struct WarpCfg { int nw, ppt, nst; };
-static const WarpCfg kWarpCfgs[] = {{16, 4, 4}, {16, 4, 3}, {8, 4, 6}, {16, 2, 6}};
+static const WarpCfg kWarpCfgs[] = {{16, 4, 4}, {16, 4, 3}, {15, 4, 2}, {16, 2, 6}};
 
 template <int XY, bool ATTR, int NW, int PPT, int NST>
 static cudaError_t warp_run(const PassArgs& a, size_t smem, cudaStream_t s, int* blocks, bool launch) {
@@ -1447,7 +1452,7 @@ static cudaError_t warp_dispatch(int ci, const PassArgs& a, size_t smem, cudaStr
   switch (ci) {
     case 0: return warp_run<XY, ATTR, 16, 4, 4>(a, smem, s, blocks, launch);
     case 1: return warp_run<XY, ATTR, 16, 4, 3>(a, smem, s, blocks, launch);
-    case 2: return warp_run<XY, ATTR, 8, 4, 6>(a, smem, s, blocks, launch);
+    case 2: return warp_run<XY, ATTR, 15, 4, 2>(a, smem, s, blocks, launch);
     default: return warp_run<XY, ATTR, 16, 2, 6>(a, smem, s, blocks, launch);
   }
 }
