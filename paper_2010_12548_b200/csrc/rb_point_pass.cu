@@ -81,7 +81,7 @@ struct PassArgs {
   unsigned long long* first_bad;
   int64_t idx_base;  // global index of point 0 (chunked host joins)
   long long* part_acc;
-  const int* scale_exp;
+  int* scale_exp;
   const int32_t* hot_region;  // global mode: hot slot -> region
   int n_hot;
   int hcopies;  // warp kernel: copies of the shared histogram (lane & (hcopies-1) picks one)
@@ -1028,7 +1028,28 @@ __global__ void __launch_bounds__(NW * 32 + 32, NW <= 8 ? 2 : 1) k_point_pass_ri
   float sc = 1.f;
   uint32_t wminb = 0, wspan = 0;
   if (ATTR) {
-    const int Sx = *a.scale_exp;
+    // binary scale of the SUM fixed point from the same strided 4096-value sample in every CTA
+    // (deterministic, identical to k_attr_scale; its loads overlap the producer's first tiles)
+    __shared__ float smax[NW];
+    float mx = 0.f;
+    const int64_t stride = a.n / 4096 > 0 ? a.n / 4096 : 1;
+    for (int64_t q = tid; q < 4096 && q * stride < a.n; q += NW * 32) {
+      const float v = fabsf(__ldg(a.attr + q * stride));
+      if (isfinite(v)) mx = fmaxf(mx, v);
+    }
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) smax[warp] = mx;
+    asm volatile("bar.sync 1, %0;" ::"r"(NW * 32) : "memory");
+    mx = 0.f;
+    for (int w2 = 0; w2 < NW; ++w2) mx = fmaxf(mx, smax[w2]);
+    int Sx = 0;
+    if (mx > 0.f) {
+      int e = 0;
+      frexpf(mx, &e);  // mx < 2^e
+      Sx = 29 - e;     // fast window [2^(e-9), 2^(e+1))
+    }
+    Sx = Sx < -96 ? -96 : (Sx > 126 ? 126 : Sx);
+    if (blockIdx.x == 0 && tid == 0) *a.scale_exp = Sx;  // for k_reduce_fixed
     sc = __int_as_float((Sx + 127) << 23);
     wminb = (uint32_t)((20 - Sx + 127) << 23);  // |w| in [2^(20-S), 2^(30-S)): exact 30-bit fixed point
     wspan = (uint32_t)((30 - Sx + 127) << 23) - wminb;
@@ -1597,12 +1618,7 @@ int point_pass(const rb_approx* A, const void* xy, int32_t dtype, int64_t n, con
     a.part_sum = (double*)((char*)scratch + rows * 8);
     a.part_cnt = (uint32_t*)((char*)scratch + rows * 16);
     int* scale = (int*)((char*)scratch + rows * 20);
-    a.scale_exp = scale;
-    if (attr) {
-      k_attr_scale<<<1, 1024, 0, s>>>(attr, n, scale);
-      RB_CUDA(cudaGetLastError());
-      ++g_launches;
-    }
+    a.scale_exp = scale;  // written by the ring kernel (CTA 0) for k_reduce_fixed
     if (tstart()) return RB_CUDA_ERROR;
     e = dtype == RB_XY_F64 ? (attr ? warp_dispatch<0, true>(wci, a, smem, s, &blocks, true)
                                    : warp_dispatch<0, false>(wci, a, smem, s, &blocks, true))
