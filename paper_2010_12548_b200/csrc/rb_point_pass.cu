@@ -87,6 +87,7 @@ struct PassArgs {
   int hcopies;  // warp kernel: copies of the shared histogram (lane & (hcopies-1) picks one)
   int hstride;  // warp kernel: words per histogram copy (== 1 mod 32: a bin's copies sit in distinct banks)
   int ablate;   // timing experiments only (RB_ABLATE): 1 skip rare path, 2 skip node level, 4 skip root
+  int fold;     // ring kernel: cap on the drain period in warp-tiles (RB_FOLD, tests); 0 = automatic
 };
 
 template <bool SMEM, bool ATTR>
@@ -959,7 +960,8 @@ __global__ void __launch_bounds__(NW * 32 + 32, NW <= 8 ? 2 : 1) k_point_pass_ri
   // total, so the low-half sums stay < 2^32 and the signed high-half sums within +-2^30 (|qv| < 2^30).
   const int C = a.hcopies, P = a.hstride;
   // (62000 leaves room for the <= 63 points a warp's rare queue carries across a drain)
-  const int FOLD = C * (62000 / (NW * WT) > 0 ? 62000 / (NW * WT) : 1);
+  int FOLD = C * (62000 / (NW * WT) > 0 ? 62000 / (NW * WT) : 1);
+  if (a.fold > 0 && a.fold < FOLD) FOLD = a.fold;
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ LevelDesc lv;
   __shared__ __align__(8) uint64_t full[NST], empty[NST];
@@ -1611,6 +1613,10 @@ int point_pass(const rb_approx* A, const void* xy, int32_t dtype, int64_t n, con
       env_ablate = e ? atoi(e) : 0;
     }
     a.ablate = env_ablate;
+    {
+      const char* e = getenv("RB_FOLD");  // read per call: tests shorten the drain period
+      a.fold = e ? atoi(e) : 0;
+    }
     void* scratch = nullptr;
     const size_t rows = (size_t)blocks * R2;
     RB_CUDA(cudaMallocAsync(&scratch, rows * 20 + 16, s));

@@ -219,3 +219,46 @@ def test_large_region_set_global_histogram(oracle_lib):
         idx = _prepared(regions, grid, mode, "trie")
         _assert_join(idx, A, xy, attr)
         _assert_join(idx, A, xy32, attr)
+
+
+@pytest.mark.parametrize("fold", ["1", "3"])
+def test_ring_drains_and_out_of_window_sums(oracle_lib, monkeypatch, fold):
+    """The ring kernel's barrier-free drains of the 16-bit fixed-point halves
+    (forced every `fold` warp-tiles via RB_FOLD), the per-warp rare queue, and
+    attribute values outside the fixed-point window (tiny, huge, zero,
+    negative) that take the float64 path: COUNT bit-exact, SUM rel 1e-6."""
+    _gpu()
+    from paper_2010_12548_b200 import workloads as W
+    from paper_2010_12548_b200.grid import level_for_bound
+
+    monkeypatch.setenv("RB_FOLD", fold)
+    w = W.c2(n=3_000_003)  # not a multiple of 4: the trailing-point path too
+    grid = w.grid.with_level(level_for_bound(w.grid, w.epsilon))
+    attr = w.attrs["fare"].copy()
+    rng = np.random.default_rng(5)
+    k = rng.choice(len(attr), 20_000, replace=False)
+    attr[k[:5000]] *= 1e-6          # below the window
+    attr[k[5000:10000]] *= 1e6      # above the window
+    attr[k[10000:15000]] = 0.0
+    attr[k[15000:]] *= -1.0         # negative values: signed fixed point
+    A, _ = oracle_approx(oracle_lib, w.regions, grid, 0)
+    idx = _prepared(w.regions, grid, 0, "trie")
+    _assert_join(idx, A, w.xy, attr)
+
+
+def test_single_hot_region_copies(oracle_lib):
+    """Every point in one region (the worst case for same-address REDs that the
+    bank-staggered histogram copies absorb): exact COUNT, SUM within 1e-6."""
+    _gpu()
+    from paper_2010_12548_b200.geometry import Polygon, RegionRecord
+
+    regions = [RegionRecord(0, Polygon([(0.0, 0.0), (0.5, 0.0), (0.5, 0.5), (0.0, 0.5)])),
+               RegionRecord(1, Polygon([(0.5, 0.5), (1.0, 0.5), (1.0, 1.0), (0.5, 1.0)]))]
+    grid = UNIT.with_level(12)
+    rng = np.random.default_rng(9)
+    xy = rng.random((2_000_000, 2)) * 0.49  # all inside region 0's interior
+    attr = rng.lognormal(2.5, 0.6, len(xy)).astype(np.float32)
+    A, _ = oracle_approx(oracle_lib, regions, grid, 0)
+    idx = _prepared(regions, grid, 0, "trie")
+    cnt = _assert_join(idx, A, xy, attr)
+    assert cnt[0, 0] == len(xy)
