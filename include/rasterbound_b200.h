@@ -174,6 +174,51 @@ int rb_exact_pip(const rb_polygons* polys, const double* px, const double* py, c
 int rb_exact_distance(const rb_polygons* polys, const double* px, const double* py, const int32_t* poly_of_point,
                       int64_t n, double* dist_out, void* stream);
 
+/* ---- point-side access path: pointindex + join_pointindex (SPEC.md:313-382,
+ * 491-499).  The reference has no FFI for these either; they
+ * replace the Python operations named below. */
+typedef struct rb_lps rb_lps; /* pointindex.LinearizedPointSet */
+typedef struct rb_rs rb_rs;   /* pointindex.RadixSplineIndex */
+
+/* pointindex.lps_build: leaf Z codes (grid level L) of n
+ * device points sorted with their permutation (stable: equal codes keep point
+ * order), float64 prefix sums (n + 1 entries, prefix[0] = 0) of n_attr device
+ * float32 attribute arrays in sorted order.  Synchronous.  An out-of-domain or
+ * NaN point gives RB_DOMAIN_ERROR with its index in *first_bad (host). */
+int rb_lps_build(const rb_grid* grid, const void* xy, int32_t xy_dtype, int64_t n, const float* const* attrs,
+                 int32_t n_attr, void* stream, rb_lps** out, int64_t* first_bad);
+/* device views: codes u64 [n], perm i64 [n], prefix f64 [n_attr][n + 1] */
+int rb_lps_info(const rb_lps* lps, int64_t* n, const uint64_t** codes, const int64_t** perm, const double** prefix,
+                int32_t* n_attr);
+void rb_lps_free(rb_lps* lps);
+
+/* pointindex.rs_build: RadixSpline over the distinct-key
+ * CDF of the codes -- spline knots with interpolation error <= max_error at
+ * every stored key, radix table over the top radix_bits of the 2L-bit code
+ * space.  radix_bits > 2L (or > 30) is RB_CONFIG_ERROR.  Synchronous. */
+int rb_rs_build(const rb_lps* lps, int32_t radix_bits, int32_t max_error, void* stream, rb_rs** out);
+/* device views: knot keys u64 / positions i64 [n_knots], radix table u32 [2^radix_bits + 1] */
+int rb_rs_info(const rb_rs* rs, int64_t* n_knots, const uint64_t** keys, const int64_t** pos, const uint32_t** table,
+               int32_t* radix_bits, int32_t* shift);
+void rb_rs_free(rb_rs* rs);
+
+/* pointindex.bounds_lookup, batched: for m intervals
+ * [lo, hi) of level-L codes (device u64), lo_pos / hi_pos (device i64) = first
+ * sorted position with code >= lo / >= hi.  rs may be NULL (binary search);
+ * with rs the result is identical.  Stream-ordered. */
+int rb_bounds_lookup(const rb_lps* lps, const rb_rs* rs, const uint64_t* lo, const uint64_t* hi, int64_t m,
+                     int64_t* lo_pos, int64_t* hi_pos, void* stream);
+
+/* query.join_pointindex over pointindex.range_aggregate
+ * (SPEC.md:355-363): covering cells (device arrays, grouped by region: region
+ * ids non-decreasing; level, Z code at that level, kind 1 = interior /
+ * 2 = boundary) -> per region alpha/beta COUNT (device int64 [n_regions*2]) and
+ * SUM of prefix attribute attr_idx (device float64 [n_regions*2]; attr_idx < 0:
+ * sums left 0).  Cells of one region must be disjoint.  Deterministic. */
+int rb_join_pointindex(const rb_lps* lps, const rb_rs* rs, int64_t n_cells, const int32_t* region,
+                       const int32_t* level, const uint64_t* code, const uint8_t* kind, int32_t n_regions,
+                       int32_t attr_idx, int64_t* cnt_out, double* sum_out, void* stream);
+
 /* Instrumentation (benchmarks): op 1 = reset counters and enable CUDA-event
  * timing of the point-pass main kernel, op 2 = reset and disable, op 0 = read
  * (synchronises the recorded events): launches of this library's point-pass

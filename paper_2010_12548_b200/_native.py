@@ -31,6 +31,8 @@ EXPORTS = (
     "rb_version", "rb_last_error", "rb_level_for_bound", "rb_approx_build", "rb_approx_stats", "rb_approx_free",
     "rb_point_pass", "rb_join_host", "rb_lookup", "rb_owner_pool", "rb_point_cells", "rb_approx_cells",
     "rb_approx_partial", "rb_exact_pip", "rb_exact_distance", "rb_index_from_cells", "rb_instrument", "rb_approx_set_hot",
+    "rb_lps_build", "rb_lps_info", "rb_lps_free", "rb_rs_build", "rb_rs_info", "rb_rs_free", "rb_bounds_lookup",
+    "rb_join_pointindex",
 )
 
 
@@ -93,6 +95,17 @@ def load() -> C.CDLL:
     L.rb_exact_distance.argtypes = [C.POINTER(Polygons), p, p, p, i64, p, p]
     L.rb_instrument.argtypes = [i32, C.POINTER(i64), C.POINTER(i64), C.POINTER(d)]
     L.rb_approx_set_hot.argtypes = [p, p, i32, p]
+    L.rb_lps_build.argtypes = [C.POINTER(Grid), p, i32, i64, p, i32, p, C.POINTER(p), C.POINTER(i64)]
+    L.rb_lps_info.argtypes = [p, C.POINTER(i64), C.POINTER(p), C.POINTER(p), C.POINTER(p), C.POINTER(i32)]
+    L.rb_lps_free.argtypes = [p]
+    L.rb_lps_free.restype = None
+    L.rb_rs_build.argtypes = [p, i32, i32, p, C.POINTER(p)]
+    L.rb_rs_info.argtypes = [p, C.POINTER(i64), C.POINTER(p), C.POINTER(p), C.POINTER(p), C.POINTER(i32),
+                             C.POINTER(i32)]
+    L.rb_rs_free.argtypes = [p]
+    L.rb_rs_free.restype = None
+    L.rb_bounds_lookup.argtypes = [p, p, p, p, i64, p, p, p]
+    L.rb_join_pointindex.argtypes = [p, p, i64, p, p, p, p, i32, i32, p, p, p]
     for name in EXPORTS:
         getattr(L, name)  # AttributeError if an export is missing
     _lib = L

@@ -195,26 +195,33 @@ class PreparedJoin:
         return self.results(cnt, sm, ps)
 
     def results(self, cnt: np.ndarray, sm: np.ndarray, points: PointSet | None = None) -> list:
-        a = self.q.agg
+        return _results(self.packed, self.q, cnt, sm, points)
+
+
+def _results(packed: PackedRegions, q: AggregationQuery, cnt: np.ndarray, sm: np.ndarray,
+             points: PointSet | None = None, nonneg: bool | None = None) -> list:
+    """RegionResult per region from [R,2] alpha/beta COUNT and SUM."""
+    a = q.agg
+    if nonneg is None:
         nonneg = True
         if a.kind != "COUNT" and points is not None:
             v = points.attrs.get(a.attr)
             if v is not None:
                 nonneg = bool((v.min() >= 0).item()) if len(v) else True
-        out = []
-        for k, rid in enumerate(self.packed.region_ids.tolist()):
-            ac, bc = int(cnt[k, 0]), int(cnt[k, 1])
-            if a.kind == "COUNT":
-                alpha, beta = ac, bc
-            elif a.kind == "SUM":
-                alpha, beta = float(sm[k, 0]), float(sm[k, 1])
-            else:
-                alpha = float(sm[k, 0]) / ac if ac else EMPTY
-                beta = float(sm[k, 1]) / bc if bc else EMPTY
-            rr = RegionResult(int(rid), alpha, beta)
-            rr.range = result_range(rr, self.q, nonneg)
-            out.append(rr)
-        return out
+    out = []
+    for k, rid in enumerate(packed.region_ids.tolist()):
+        ac, bc = int(cnt[k, 0]), int(cnt[k, 1])
+        if a.kind == "COUNT":
+            alpha, beta = ac, bc
+        elif a.kind == "SUM":
+            alpha, beta = float(sm[k, 0]), float(sm[k, 1])
+        else:
+            alpha = float(sm[k, 0]) / ac if ac else EMPTY
+            beta = float(sm[k, 1]) / bc if bc else EMPTY
+        rr = RegionResult(int(rid), alpha, beta)
+        rr.range = result_range(rr, q, nonneg)
+        out.append(rr)
+    return out
 
 
 def join_act(points, regions, q: AggregationQuery, cfg: GridConfig | None = None, layout: str = "trie",
@@ -226,6 +233,100 @@ def join_act(points, regions, q: AggregationQuery, cfg: GridConfig | None = None
     packed = pack_regions(regions)
     cfg = _grid_for(ps, packed, cfg)
     return PreparedJoin(packed, q, cfg, layout=layout, radix_width=radix_width).run(ps)
+
+
+def _region_cells(packed: PackedRegions, index: ApproxIndex, L: int):
+    """Disjoint covering cells per region: a multi-polygon
+    region's coverings are unioned, a cell inside a coarser cell of the same
+    region is dropped (the coarser wins), identical cells keep interior if any
+    polygon has it interior.  Returns (region, level, code, kind) grouped by region."""
+    poly, level, code, kind = index.cells()
+    region = packed.poly_region[poly].astype(np.int32)
+    counts = np.bincount(packed.poly_region, minlength=packed.n_regions)
+    multi = counts[region] > 1
+    if multi.any():
+        keep = ~multi
+        lv = level.astype(np.int64)
+        lo = code.astype(np.uint64) << (2 * (L - lv)).astype(np.uint64)
+        hi = (code.astype(np.uint64) + np.uint64(1)) << (2 * (L - lv)).astype(np.uint64)
+        idx = np.nonzero(multi)[0]
+        # per region: by start, larger cells first, interior before boundary
+        order = idx[np.lexsort((kind[idx], lv[idx], lo[idx], region[idx]))]
+        kind = kind.copy()
+        cur_r, cur_hi, cur_j = -1, np.uint64(0), -1
+        for j in order.tolist():
+            r = int(region[j])
+            if r == cur_r and lo[j] < cur_hi:  # nested in (or identical to) the kept cell
+                if lo[j] == lo[cur_j] and hi[j] == cur_hi and kind[j] == 1:
+                    kind[cur_j] = 1
+                continue
+            keep[j] = True
+            cur_r, cur_hi, cur_j = r, hi[j], j
+        region, level, code, kind = region[keep], level[keep], code[keep], kind[keep]
+    o = np.argsort(region, kind="stable")
+    return region[o], level[o].astype(np.int32), code[o], kind[o].astype(np.uint8)
+
+
+class PreparedPointIndexJoin:
+    """The region side of join_pointindex, built once per (regions, epsilon,
+    mode): the hierarchical coverings as disjoint per-region cells on the
+    device.  run() answers the query from a point index."""
+
+    def __init__(self, regions, q: AggregationQuery, grid: GridConfig):
+        torch = N.require_cuda()
+        if q.filter is not None:
+            raise E.ConfigError("join_pointindex aggregates prefix sums over all points; filters need join_act")
+        self.q = q
+        self.packed = regions if isinstance(regions, PackedRegions) else pack_regions(regions)
+        L = level_for_bound(grid, q.epsilon)
+        self.grid = grid.with_level(L)
+        index = ApproxIndex(self.packed, self.grid, int(q.mode), layout="trie", keep_cells=True)
+        region, level, code, kind = _region_cells(self.packed, index, L)
+        del index
+        self.n_cells = int(len(region))
+        self._region = torch.as_tensor(region).cuda()
+        self._level = torch.as_tensor(level).cuda()
+        self._code = torch.as_tensor(code.view(np.int64)).cuda()
+        self._kind = torch.as_tensor(kind).cuda()
+
+    def run_device(self, lps, rs=None, stream=None):
+        """Per-region [R,2] alpha/beta COUNT (int64) and SUM (float64) device tensors."""
+        torch = N.require_cuda()
+        if lps.grid.max_level != self.grid.max_level:
+            raise E.ConfigError(f"point index built at level {lps.grid.max_level}, "
+                                f"query epsilon needs level {self.grid.max_level}")
+        a = self.q.agg
+        attr_idx = -1
+        if a.kind != "COUNT":
+            if a.attr not in lps.attrs:
+                raise E.SchemaError(f"attribute {a.attr!r} has no prefix array in the point index (SPEC.md:359)")
+            attr_idx = lps.attrs.index(a.attr)
+        R = self.packed.n_regions
+        cnt = torch.zeros((R, 2), dtype=torch.int64, device="cuda")
+        sm = torch.zeros((R, 2), dtype=torch.float64, device="cuda")
+        N.check(N.load().rb_join_pointindex(lps._h, rs._h if rs is not None else None, self.n_cells,
+                                            self._region.data_ptr(), self._level.data_ptr(), self._code.data_ptr(),
+                                            self._kind.data_ptr(), R, attr_idx, cnt.data_ptr(), sm.data_ptr(),
+                                            N.stream_ptr(stream)), "join_pointindex")
+        return cnt, sm
+
+    def run(self, lps, rs=None) -> list:
+        cnt, sm = self.run_device(lps, rs)
+        a = self.q.agg
+        nonneg = True
+        if a.kind != "COUNT":
+            pre = lps.prefix(a.attr)
+            nonneg = bool((pre[1:] - pre[:-1] >= 0).all().item()) if lps.n else True
+        return _results(self.packed, self.q, cnt.cpu().numpy(), sm.cpu().numpy(), nonneg=nonneg)
+
+
+def join_pointindex(lps, rs, regions, q: AggregationQuery) -> list:
+    """per region, its covering (hierarchical raster at the
+    query's epsilon and mode) as cell intervals, each aggregated from the point
+    index with two lower-bound lookups and a prefix difference
+    (pointindex.range_aggregate); beta from the boundary cells only.  Equals
+    join_act exactly for COUNT."""
+    return PreparedPointIndexJoin(regions, q, lps.grid).run(lps, rs)
 
 
 CANVAS_MAX_LEVEL = 17
@@ -246,5 +347,6 @@ def join_canvas(points, regions, q: AggregationQuery, cfg: GridConfig | None = N
 
 __all__ = [
     "Agg", "AggregationQuery", "RegionResult", "result_range", "PreparedJoin", "join_act", "join_canvas",
+    "join_pointindex", "PreparedPointIndexJoin",
     "UNAVAILABLE", "EMPTY",
 ]

@@ -78,6 +78,22 @@ EXAMPLES = [
      "epsilon": R2 / 2, "points": [[0.2, 0.7], [0.8, 0.2]], "expect": [[[0, "I"]], [[1, "I"]]]},
     {"op": "act_lookup", "spec": "SPEC.md:291", "regions": {}, "epsilon": R2, "points": [[0.3, 0.3]],
      "expect": [[]]},
+    # pointindex.lps_build: leaf codes at L=1 over the unit square (code 0 = (0,0), 1 = (1,0),
+    # 2 = (0,1), 3 = (1,1)); counts per code [1, 2, 0, 3] -> COUNT prefix [0, 1, 3, 3, 6]
+    {"op": "lps_build", "spec": "SPEC.md:334", "L": 1,
+     "points": [[0.1, 0.1], [0.6, 0.2], [0.9, 0.4], [0.7, 0.7], [0.8, 0.9], [0.55, 0.6]],
+     "expect_codes": [0, 1, 1, 3, 3, 3], "expect_count_prefix": [0, 1, 3, 3, 6]},
+    {"op": "lps_build", "spec": "SPEC.md:333", "L": 3, "points": [], "expect_codes": [], "expect_prefix": [0]},
+    {"op": "lps_build", "spec": "SPEC.md:335", "L": 4, "points": [[0.3, 0.3], [0.3, 0.3]],
+     "expect_codes_equal_adjacent": True},
+    # pointindex.bounds_lookup
+    {"op": "bounds_lookup", "spec": "SPEC.md:352", "codes": [2, 4, 4, 7, 9, 12], "iv": [0, 1 << 40],
+     "expect": [0, 6]},
+    {"op": "bounds_lookup", "spec": "SPEC.md:353", "codes": [2, 4, 4, 7, 9, 12], "iv": [4, 8], "expect": [1, 4]},
+    {"op": "bounds_lookup", "spec": "SPEC.md:354", "codes": [2, 4, 4, 7, 9, 12], "iv": [5, 5], "expect": [3, 3]},
+    # pointindex.range_aggregate: counts per code [1, 2, 0, 3], cells covering codes {1, 2} -> 2
+    {"op": "range_aggregate", "spec": "SPEC.md:361", "codes": [0, 1, 1, 3, 3, 3], "cells": [[1, 3]], "expect": 2},
+    {"op": "range_aggregate", "spec": "SPEC.md:362", "codes": [0, 1, 1, 3, 3, 3], "cells": [[0, 4]], "expect": 6},
     # query.join_act
     {"op": "join_act", "spec": "SPEC.md:488", "outer": UNIT, "epsilon": 0.1,
      "points": [[0.1, 0.1], [0.2, 0.9], [0.5, 0.5], [0.7, 0.3], [0.9, 0.9], [0.05, 0.6], [0.6, 0.05]],

@@ -133,10 +133,11 @@ def test_join_act(oracle_lib, e):
 
 
 def test_all_examples_covered():
-    """Every golden example is exercised by a CPU test here or in test_host_api.py."""
+    """Every golden example is exercised by a CPU test here, in test_host_api.py
+    or in test_pointindex_oracle.py."""
     ops = {e["op"] for e in EX}
     covered = {"level_for_bound", "z_encode", "point_to_cell", "point_in_polygon", "distance_to_boundary",
                "classify_cell", "rasterize_hierarchical", "rasterize_uniform", "act_lookup", "join_act",
                "cell_interval", "children", "parent", "mbr_of", "result_range", "hausdorff_distance",
-               "hausdorff_squares"}
+               "hausdorff_squares", "lps_build", "bounds_lookup", "range_aggregate"}
     assert ops <= covered
