@@ -219,6 +219,56 @@ int rb_join_pointindex(const rb_lps* lps, const rb_rs* rs, int64_t n_cells, cons
                        const int32_t* level, const uint64_t* code, const uint8_t* kind, int32_t n_regions,
                        int32_t attr_idx, int64_t* cnt_out, double* sum_out, void* stream);
 
+/* ---- canvas algebra (section 4) and the Bounded
+ * Raster Join plan.  A canvas tile is a dense row-major
+ * 2^level x 2^level block of the level-L leaf grid at pixel offset (x0, y0);
+ * pixel (ix, iy) is leaf z_encode(ix, iy, L).  Caller-owned
+ * device channels: */
+typedef struct rb_canvas_desc {
+  int32_t level;  /* tile side 2^level pixels (<= 16) */
+  int64_t x0, y0; /* pixel offset of the tile in the level-L grid */
+  int32_t n_sum;  /* SUM channels */
+  int64_t* count; /* [2^(2 level)] point count */
+  double* sums;   /* [n_sum][2^(2 level)] */
+  int32_t* region; /* [2^(2 level)] region id, -1 = none */
+  uint8_t* flags;  /* [2^(2 level)] bit 0 non-empty, bit 1 boundary cell */
+} rb_canvas_desc;
+
+#define RB_BLEND_SUM 0
+#define RB_BLEND_OVERWRITE 1
+#define RB_BLEND_MAX 2
+#define RB_MASK_NONEMPTY 0
+#define RB_MASK_REGION_EQ 1     /* arg = region id */
+#define RB_MASK_BOUNDARY_ONLY 2
+#define RB_MASK_COUNT_GT 3      /* arg = threshold */
+#define RB_MASK_COVERED_BY 4    /* by = region canvas: keep pixels it covers (inherit its boundary flag) */
+#define RB_MASK_BOUNDARY_OF 5   /* by = region canvas: keep pixels on its boundary cells */
+
+int rb_canvas_clear(rb_canvas_desc* c, void* stream);
+/* canvas.render_points: per pixel COUNT and the first n_sum
+ * prefix attributes of the point index (exact per-pixel reductions of the
+ * sorted points, deterministic); out-of-tile points are skipped. */
+int rb_canvas_render_points(const rb_lps* lps, rb_canvas_desc* out, void* stream);
+/* canvas.render_polygon from a region's covering cells
+ * (device arrays: level, code at that level, kind 1/2): every leaf pixel of a
+ * cell gets region_id, the non-empty flag, and the boundary flag for kind 2.
+ * clear = 1 empties the tile first. */
+int rb_canvas_render_cells(int64_t n_cells, const int32_t* level, const uint64_t* code, const uint8_t* kind, int32_t L,
+                           int32_t region_id, int32_t clear, rb_canvas_desc* out, void* stream);
+/* canvas.blend: pixel-wise fn; empty (.) x = x. */
+int rb_canvas_blend(const rb_canvas_desc* a, const rb_canvas_desc* b, int32_t fn, rb_canvas_desc* out, void* stream);
+/* canvas.mask: pixels failing the predicate become empty. */
+int rb_canvas_mask(const rb_canvas_desc* a, int32_t pred, int64_t arg, const rb_canvas_desc* by, rb_canvas_desc* out,
+                   void* stream);
+/* canvas.affine: integer translation (dx, dy) then axis
+ * flips; pixels mapped outside drop.  out must not alias a.  Non-integer
+ * transforms are rejected by the caller (UnsupportedTransform). */
+int rb_canvas_affine(const rb_canvas_desc* a, int64_t dx, int64_t dy, int32_t flip_x, int32_t flip_y,
+                     rb_canvas_desc* out, void* stream);
+/* reduce over non-empty pixels: cnt_out (device int64 [2]: all, boundary
+ * pixels), sum_out (device float64 [n_sum][2]).  Fixed-order, deterministic. */
+int rb_canvas_reduce(const rb_canvas_desc* a, int64_t* cnt_out, double* sum_out, void* stream);
+
 /* Instrumentation (benchmarks): op 1 = reset counters and enable CUDA-event
  * timing of the point-pass main kernel, op 2 = reset and disable, op 0 = read
  * (synchronises the recorded events): launches of this library's point-pass

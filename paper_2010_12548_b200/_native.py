@@ -32,7 +32,8 @@ EXPORTS = (
     "rb_point_pass", "rb_join_host", "rb_lookup", "rb_owner_pool", "rb_point_cells", "rb_approx_cells",
     "rb_approx_partial", "rb_exact_pip", "rb_exact_distance", "rb_index_from_cells", "rb_instrument", "rb_approx_set_hot",
     "rb_lps_build", "rb_lps_info", "rb_lps_free", "rb_rs_build", "rb_rs_info", "rb_rs_free", "rb_bounds_lookup",
-    "rb_join_pointindex",
+    "rb_join_pointindex", "rb_canvas_clear", "rb_canvas_render_points", "rb_canvas_render_cells", "rb_canvas_blend",
+    "rb_canvas_mask", "rb_canvas_affine", "rb_canvas_reduce",
 )
 
 
@@ -60,6 +61,11 @@ class Stats(C.Structure):
 
     def as_dict(self) -> dict:
         return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+class CanvasDesc(C.Structure):
+    _fields_ = [("level", C.c_int32), ("x0", C.c_int64), ("y0", C.c_int64), ("n_sum", C.c_int32),
+                ("count", C.c_void_p), ("sums", C.c_void_p), ("region", C.c_void_p), ("flags", C.c_void_p)]
 
 
 _lib = None
@@ -106,6 +112,14 @@ def load() -> C.CDLL:
     L.rb_rs_free.restype = None
     L.rb_bounds_lookup.argtypes = [p, p, p, p, i64, p, p, p]
     L.rb_join_pointindex.argtypes = [p, p, i64, p, p, p, p, i32, i32, p, p, p]
+    cd = C.POINTER(CanvasDesc)
+    L.rb_canvas_clear.argtypes = [cd, p]
+    L.rb_canvas_render_points.argtypes = [p, cd, p]
+    L.rb_canvas_render_cells.argtypes = [i64, p, p, p, i32, i32, i32, cd, p]
+    L.rb_canvas_blend.argtypes = [cd, cd, i32, cd, p]
+    L.rb_canvas_mask.argtypes = [cd, i32, i64, cd, cd, p]
+    L.rb_canvas_affine.argtypes = [cd, i64, i64, i32, i32, cd, p]
+    L.rb_canvas_reduce.argtypes = [cd, p, p, p]
     for name in EXPORTS:
         getattr(L, name)  # AttributeError if an export is missing
     _lib = L

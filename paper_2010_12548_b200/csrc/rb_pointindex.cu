@@ -273,6 +273,20 @@ static RsView view_of(const rb_rs* rs) {
 
 }  // namespace rb
 
+namespace rb {
+// internal view for the canvas module (rb_canvas.cu)
+int lps_view(const rb_lps* L, int64_t* n, const uint64_t** codes, const double** prefix, int32_t* n_attr,
+             int32_t* level) {
+  if (!L) return fail(RB_CONFIG_ERROR, "null point index");
+  *n = L->n;
+  *codes = L->codes.as<uint64_t>();
+  *prefix = L->prefix.as<double>();
+  *n_attr = L->n_attr;
+  *level = L->grid.max_level;
+  return RB_OK;
+}
+}  // namespace rb
+
 using namespace rb;
 
 extern "C" int rb_lps_build(const rb_grid* grid, const void* xy, int32_t xy_dtype, int64_t n, const float* const* attrs,

@@ -332,13 +332,24 @@ def join_pointindex(lps, rs, regions, q: AggregationQuery) -> list:
 CANVAS_MAX_LEVEL = 17
 
 
-def join_canvas(points, regions, q: AggregationQuery, cfg: GridConfig | None = None) -> list:
+def join_canvas(points, regions, q: AggregationQuery, cfg: GridConfig | None = None, plan: str = "fused") -> list:
     """SPEC.md:500-508 (Bounded Raster Join): point canvas x region canvases at
-    the resolution chosen from epsilon -- evaluated as one fused pass over the
-    dense canvas layout (pixel = leaf cell)."""
+    the resolution chosen from epsilon.  plan="fused" (default) evaluates it as
+    one pass over the dense canvas layout (pixel = leaf cell, SPEC.md:391);
+    plan="algebra" runs the literal canvas plan (canvas.brj: render_points,
+    per region render_polygon -> mask -> reduce, tiled at 2^13 per side)."""
     ps = as_point_set(points)
     packed = pack_regions(regions)
     cfg = _grid_for(ps, packed, cfg)
+    if plan == "algebra":
+        from .canvas import brj
+
+        if q.filter is not None:
+            ps = _apply_filter(ps, q.filter)
+        cnt, sm = brj(ps, packed, q, cfg)
+        return _results(packed, q, cnt, sm, ps)
+    if plan != "fused":
+        raise E.ConfigError(f"unknown join_canvas plan {plan!r} (fused | algebra)")
     L = level_for_bound(cfg, q.epsilon)
     if L > CANVAS_MAX_LEVEL:
         raise E.CapacityError(f"canvas resolution 2^{L} exceeds the dense limit 2^{CANVAS_MAX_LEVEL}; use join_act")
