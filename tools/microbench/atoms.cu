@@ -22,6 +22,21 @@ __global__ void k(unsigned* out, int iters, uint32_t nb) {
   __syncthreads();
   for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) if (h[i] == 0xdeadbeef) out[0] = 1;
 }
+// one 64-bit shared atomicAdd per point (compiles to a CAS loop): count in the
+// high bits, fixed-point value in the low bits
+__global__ void k64(unsigned* out, int iters, uint32_t nb) {
+  extern __shared__ unsigned long long h64[];
+  for (uint32_t i = threadIdx.x; i < nb * 8; i += blockDim.x) h64[i] = 0;
+  __syncthreads();
+  uint32_t s = 0x9e3779b9u * (blockIdx.x * blockDim.x + threadIdx.x + 1);
+  const uint32_t copy = threadIdx.x & 7;
+  for (int it = 0; it < iters; ++it) {
+    uint32_t b = (xs(s) & 0xffff) % nb;
+    atomicAdd(&h64[b * 8 + copy], (1ull << 46) + (s & 0xfffff));
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) if (h64[i] == 0xdeadbeef) out[0] = 1;
+}
 // same loop without atomics (to subtract the RNG/loop cost)
 __global__ void k0(unsigned* out, int iters, uint32_t nb) {
   uint32_t s = 0x9e3779b9u * (blockIdx.x * blockDim.x + threadIdx.x + 1), acc = 0;
@@ -34,10 +49,10 @@ int main() {
   unsigned* d; cudaMalloc(&d, 16);
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
   const int iters = 4000;
-  for (uint32_t nb : {520u, 80000u / 12u * 2u}) for (int wps : {8, 16, 32}) for (int na = 0; na <= 3; ++na) {
+  for (uint32_t nb : {520u, 2000u}) for (int wps : {16}) for (int na = 1; na <= 4; ++na) {
     int threads = wps * 32;
-    size_t smem = nb * 12;
-    void (*kern)(unsigned*, int, uint32_t) = na == 0 ? k0 : na == 1 ? k<1> : na == 2 ? k<2> : k<3>;
+    size_t smem = na == 4 ? nb * 64 : nb * 12;
+    void (*kern)(unsigned*, int, uint32_t) = na == 4 ? k64 : na == 1 ? k<1> : na == 2 ? k<2> : k<3>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     kern<<<sms, threads, na ? smem : 0>>>(d, iters, nb);
     cudaEventRecord(a);
