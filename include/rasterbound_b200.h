@@ -192,6 +192,11 @@ int rb_lps_info(const rb_lps* lps, int64_t* n, const uint64_t** codes, const int
                 int32_t* n_attr);
 void rb_lps_free(rb_lps* lps);
 
+/* point index file load: a LinearizedPointSet from its arrays
+ * (host or device memory; copied). */
+int rb_lps_from_arrays(const rb_grid* grid, int64_t n, const uint64_t* codes, const int64_t* perm, const double* prefix,
+                       int32_t n_attr, void* stream, rb_lps** out);
+
 /* pointindex.rs_build: RadixSpline over the distinct-key
  * CDF of the codes -- spline knots with interpolation error <= max_error at
  * every stored key, radix table over the top radix_bits of the 2L-bit code
@@ -201,6 +206,9 @@ int rb_rs_build(const rb_lps* lps, int32_t radix_bits, int32_t max_error, void* 
 int rb_rs_info(const rb_rs* rs, int64_t* n_knots, const uint64_t** keys, const int64_t** pos, const uint32_t** table,
                int32_t* radix_bits, int32_t* shift);
 void rb_rs_free(rb_rs* rs);
+/* RadixSpline from stored knots and radix table (host or device; copied) */
+int rb_rs_from_arrays(const rb_lps* lps, int32_t radix_bits, int32_t max_error, int64_t n_knots, const uint64_t* keys,
+                      const int64_t* pos, const uint32_t* table, void* stream, rb_rs** out);
 
 /* pointindex.bounds_lookup, batched: for m intervals
  * [lo, hi) of level-L codes (device u64), lo_pos / hi_pos (device i64) = first

@@ -16,6 +16,7 @@ __version__ = "0.1.0"
 def __getattr__(name):
     import importlib
 
-    if name in ("geometry", "grid", "raster", "act", "query", "engine", "workloads", "_native", "pointindex", "canvas"):
+    if name in ("geometry", "grid", "raster", "act", "query", "engine", "workloads", "_native", "pointindex", "canvas",
+                "formats", "cli"):
         return importlib.import_module(f".{name}", __name__)
     raise AttributeError(name)

@@ -72,6 +72,51 @@ def act_build(coverings, radix_width: int = 8, root_level: int = -1, layout: str
     return AdaptiveCellTrie(radix_width, g0, np.asarray(ids, np.int64), idx)
 
 
+def _from_cells(grid: GridConfig, radix_width: int, region_ids, levels, codes, kinds,
+                layout: str = "trie") -> AdaptiveCellTrie:
+    """Index from explicit (region id, level, code, kind) cells (one covering per region)."""
+    torch = N.require_cuda()
+    region_ids = np.asarray(region_ids, np.int64)
+    ids = sorted({int(r) for r in region_ids.tolist()})
+    dense = {rid: k for k, rid in enumerate(ids)}
+    cov = np.array([dense[int(r)] for r in region_ids.tolist()], np.int32)
+    cov_region = np.arange(len(ids), dtype=np.int32)
+    d = lambda a: torch.as_tensor(np.ascontiguousarray(a) if len(a) else np.zeros(1, a.dtype)).to("cuda")  # noqa
+    t_cov, t_lv = d(cov), d(np.asarray(levels, np.uint8))
+    t_code, t_kind = d(np.asarray(codes, np.uint64).view(np.int64)), d(np.asarray(kinds, np.uint8))
+    t_reg = d(cov_region)
+    opts = N.BuildOpts(0, {"trie": N.LAYOUT_TRIE, "dense": N.LAYOUT_DENSE}[layout], radix_width, -1, 0)
+    h = C.c_void_p()
+    N.check(N.load().rb_index_from_cells(C.byref(grid.native()), len(cov), t_cov.data_ptr(), t_lv.data_ptr(),
+                                         t_code.data_ptr(), t_kind.data_ptr(), t_reg.data_ptr(), len(ids), len(ids),
+                                         C.byref(opts), N.stream_ptr(), C.byref(h)), "act load")
+    idx = ApproxIndex.from_handle(h, grid, len(ids), layout, radix_width)
+    return AdaptiveCellTrie(radix_width, grid, np.asarray(ids, np.int64), idx)
+
+
+def save_act(path: str, coverings, radix_width: int = 8) -> None:
+    """ACT file: versioned magic, radix_width, grid, then the
+    covering cells the device index is rebuilt from (formats.write_act)."""
+    from .formats import write_act
+
+    coverings = list(coverings)
+    if not coverings:
+        raise E.ConfigError("no coverings to save")
+    rid = np.concatenate([np.full(r.n_cells, int(r.region_id), np.int64) for r in coverings])
+    lv = np.concatenate([r.levels for r in coverings])
+    code = np.concatenate([r.codes for r in coverings])
+    kind = np.concatenate([r.kinds for r in coverings])
+    write_act(path, coverings[0].grid, radix_width, rid, lv, code, kind)
+
+
+def load_act(path: str, layout: str = "trie") -> AdaptiveCellTrie:
+    """Rebuild the index saved by save_act (identical lookups)."""
+    from .formats import read_act
+
+    grid, rw, rid, lv, code, kind = read_act(path)
+    return _from_cells(grid, rw, rid, lv, code, kind, layout)
+
+
 def act_lookup_many(t: AdaptiveCellTrie, xy) -> list[set]:
     """Batched act_lookup: per point the set of (region_id, 'I'|'B')."""
     a = np.asarray(xy.cpu().numpy() if hasattr(xy, "cpu") else xy)
@@ -90,4 +135,4 @@ def act_lookup(t: AdaptiveCellTrie, p: Point2D) -> set:
     return act_lookup_many(t, np.array([[p.x, p.y]], np.float64))[0]
 
 
-__all__ = ["AdaptiveCellTrie", "act_build", "act_lookup", "act_lookup_many"]
+__all__ = ["AdaptiveCellTrie", "act_build", "act_lookup", "act_lookup_many", "save_act", "load_act"]

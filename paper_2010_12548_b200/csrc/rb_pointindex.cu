@@ -519,3 +519,54 @@ extern "C" int rb_join_pointindex(const rb_lps* L, const rb_rs* R, int64_t n_cel
   }
   return RB_OK;
 }
+
+extern "C" int rb_lps_from_arrays(const rb_grid* grid, int64_t n, const uint64_t* codes, const int64_t* perm,
+                                  const double* prefix, int32_t n_attr, void* stream, rb_lps** out) {
+  if (!grid || !out || n < 0 || n_attr < 0) return fail(RB_CONFIG_ERROR, "invalid argument");
+  if (n > 0 && (!codes || !perm)) return fail(RB_CONFIG_ERROR, "null arrays");
+  if (n_attr > 0 && !prefix) return fail(RB_CONFIG_ERROR, "null prefix arrays");
+  cudaStream_t s = (cudaStream_t)stream;
+  auto* L = new rb_lps();
+  L->grid = *grid;
+  L->n = n;
+  L->n_attr = n_attr;
+  auto bail = [&](int st) { delete L; return st; };
+  if (L->codes.alloc(std::max<int64_t>(n, 1) * 8) || L->perm.alloc(std::max<int64_t>(n, 1) * 8) ||
+      L->prefix.alloc(std::max<int32_t>(n_attr, 1) * (n + 1) * 8))
+    return bail(fail(RB_CAPACITY_ERROR, "out of device memory for the point index"));
+  cudaError_t e = cudaSuccess;
+  if (n) e = cudaMemcpyAsync(L->codes.p, codes, n * 8, cudaMemcpyDefault, s);
+  if (!e && n) e = cudaMemcpyAsync(L->perm.p, perm, n * 8, cudaMemcpyDefault, s);
+  if (!e && n_attr) e = cudaMemcpyAsync(L->prefix.p, prefix, (size_t)n_attr * (n + 1) * 8, cudaMemcpyDefault, s);
+  if (!e) e = cudaStreamSynchronize(s);
+  if (e) return bail(cuda_fail(e, "lps from arrays"));
+  *out = L;
+  return RB_OK;
+}
+
+extern "C" int rb_rs_from_arrays(const rb_lps* L, int32_t radix_bits, int32_t max_error, int64_t n_knots,
+                                 const uint64_t* keys, const int64_t* pos, const uint32_t* table, void* stream,
+                                 rb_rs** out) {
+  if (!L || !out || n_knots < 0) return fail(RB_CONFIG_ERROR, "invalid argument");
+  const int width = 2 * L->grid.max_level;
+  if (radix_bits < 0 || radix_bits > width || radix_bits > 30) return fail(RB_CONFIG_ERROR, "radix_bits out of range");
+  cudaStream_t s = (cudaStream_t)stream;
+  auto* R = new rb_rs();
+  R->radix_bits = radix_bits;
+  R->shift = width - radix_bits;
+  R->max_error = max_error;
+  R->n_knots = n_knots;
+  auto bail = [&](int st) { delete R; return st; };
+  const int64_t nslots = ((int64_t)1 << radix_bits) + 1;
+  if (R->keys.alloc(std::max<int64_t>(n_knots, 1) * 8) || R->pos.alloc(std::max<int64_t>(n_knots, 1) * 8) ||
+      R->table.alloc(nslots * 4))
+    return bail(fail(RB_CAPACITY_ERROR, "out of device memory for the spline"));
+  cudaError_t e = cudaSuccess;
+  if (n_knots) e = cudaMemcpyAsync(R->keys.p, keys, n_knots * 8, cudaMemcpyDefault, s);
+  if (!e && n_knots) e = cudaMemcpyAsync(R->pos.p, pos, n_knots * 8, cudaMemcpyDefault, s);
+  if (!e) e = cudaMemcpyAsync(R->table.p, table, nslots * 4, cudaMemcpyDefault, s);
+  if (!e) e = cudaStreamSynchronize(s);
+  if (e) return bail(cuda_fail(e, "rs from arrays"));
+  *out = R;
+  return RB_OK;
+}

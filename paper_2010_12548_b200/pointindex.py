@@ -189,6 +189,41 @@ def rs_build(lps: LinearizedPointSet, radix_bits: int | None = None, max_error: 
     return RadixSplineIndex(h, lps, max_error)
 
 
+def save_point_index(path: str, lps: LinearizedPointSet, rs: RadixSplineIndex | None = None) -> None:
+    """Index file: codes + prefix arrays + spline knots, versioned."""
+    from .formats import write_point_index
+
+    write_point_index(path, lps, rs)
+
+
+def load_point_index(path: str):
+    """-> (LinearizedPointSet, RadixSplineIndex | None) from save_point_index."""
+    from .formats import read_point_index
+
+    d = read_point_index(path)
+    lib = N.load()
+    n = len(d["codes"])
+    codes = np.ascontiguousarray(d["codes"])
+    perm = np.ascontiguousarray(d["perm"])
+    pre = np.ascontiguousarray(np.concatenate([d["prefix"][a] for a in d["attrs"]])) if d["attrs"] else \
+        np.zeros(1, np.float64)
+    h = C.c_void_p()
+    N.check(lib.rb_lps_from_arrays(C.byref(d["grid"].native()), n, codes.ctypes.data, perm.ctypes.data,
+                                   pre.ctypes.data, len(d["attrs"]), N.stream_ptr(), C.byref(h)), "load_point_index")
+    lps = LinearizedPointSet(h, d["grid"], tuple(d["attrs"]))
+    rs = None
+    if d["radix_bits"] >= 0:
+        keys = np.ascontiguousarray(d["keys"])
+        pos = np.ascontiguousarray(d["pos"])
+        tab = np.ascontiguousarray(d["table"])
+        hr = C.c_void_p()
+        N.check(lib.rb_rs_from_arrays(lps._h, d["radix_bits"], d["max_error"], len(keys), keys.ctypes.data,
+                                      pos.ctypes.data, tab.ctypes.data, N.stream_ptr(), C.byref(hr)),
+                "load_point_index")
+        rs = RadixSplineIndex(hr, lps, d["max_error"])
+    return lps, rs
+
+
 def _intervals(iv):
     torch = N.require_cuda()
     if isinstance(iv, CellInterval):
@@ -239,4 +274,4 @@ def range_aggregate(lps: LinearizedPointSet, rs: RadixSplineIndex | None, cells,
 
 
 __all__ = ["LinearizedPointSet", "RadixSplineIndex", "lps_build", "rs_build", "bounds_lookup", "range_aggregate",
-           "EMPTY"]
+           "save_point_index", "load_point_index", "EMPTY"]
