@@ -7,7 +7,7 @@
 
 One step = one point pass over this rank's batch of synthetic points (inputs
 resident in HBM, approximation prebuilt and replicated on every GPU), plus
-the NCCL all-reduce of the per-region [R,2] int64 COUNT and float64 SUM when
+one NCCL all-reduce of the per-region partials packed as float64 [R,4] when
 N > 1 (weak scaling: every rank owns its own batch, seed = 0 + rank).
 Rank 0 prints ONE JSON line.  See DESIGN.md "Measurement".
 """
@@ -272,7 +272,7 @@ def run_ours(a):
                        "epsilon": w.epsilon, "max_level": grid.max_level, "mode": "CONSERVATIVE",
                        "index": layout, "root_level": st["root_level"], "index_bytes": st["index_bytes"],
                        "build_ms": round(st["build_ms"], 1), "parallelism": f"dp{world} (points sharded, "
-                       "approximation replicated, NCCL all-reduce of [R,2] COUNT/SUM)",
+                       "approximation replicated, one NCCL all-reduce of the packed [R,4] f64 COUNT/SUM)",
                        "l2": f"inputs {n * C['bpp'] / 1e9:.1f} GB per pass > 126 MB L2; no flush needed"},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": sampler.summary(), "parity_vs_oracle": parity,
