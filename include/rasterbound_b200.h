@@ -277,6 +277,22 @@ int rb_canvas_affine(const rb_canvas_desc* a, int64_t dx, int64_t dy, int32_t fl
  * pixels), sum_out (device float64 [n_sum][2]).  Fixed-order, deterministic. */
 int rb_canvas_reduce(const rb_canvas_desc* a, int64_t* cnt_out, double* sum_out, void* stream);
 
+/* The complete epsilon validator (K5): for EVERY point, the
+ * approximate owner regions (index lookup) against the exact owner regions
+ * (point_in_polygon over the candidate polygons of its bucket: a uniform
+ * n_buckets_side^2 grid of side bucket_side at (bucket_x0, bucket_y0), CSR
+ * lists bucket_off [n^2+1] / bucket_poly of the polygons whose MBR expanded by
+ * epsilon meets the bucket; poly_mbr = device f64 [n_polygons][4] xmin ymin
+ * xmax ymax).  Each region in only one of the two sets is a mismatch whose
+ * distance to the region's boundary must be <= epsilon.  out6 (host) = points,
+ * mismatched points, false positives, false negatives, violations (distance >
+ * epsilon), owner-set overflows; *max_dist (host) = largest mismatch distance.
+ * All polygon and bucket arrays are device arrays.  Synchronous. */
+int rb_validate_full(const rb_approx* a, const rb_polygons* polys, const double* poly_mbr, const int32_t* bucket_off,
+                     const int32_t* bucket_poly, int32_t n_buckets_side, double bucket_x0, double bucket_y0,
+                     double bucket_side, const void* xy, int32_t xy_dtype, int64_t n, double epsilon, int64_t* out6,
+                     double* max_dist, void* stream);
+
 /* Instrumentation (benchmarks): op 1 = reset counters and enable CUDA-event
  * timing of the point-pass main kernel, op 2 = reset and disable, op 0 = read
  * (synchronises the recorded events): launches of this library's point-pass

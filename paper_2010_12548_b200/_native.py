@@ -34,6 +34,7 @@ EXPORTS = (
     "rb_lps_build", "rb_lps_info", "rb_lps_free", "rb_rs_build", "rb_rs_info", "rb_rs_free", "rb_bounds_lookup",
     "rb_join_pointindex", "rb_canvas_clear", "rb_canvas_render_points", "rb_canvas_render_cells", "rb_canvas_blend",
     "rb_canvas_mask", "rb_canvas_affine", "rb_canvas_reduce", "rb_lps_from_arrays", "rb_rs_from_arrays",
+    "rb_validate_full",
 )
 
 
@@ -111,6 +112,8 @@ def load() -> C.CDLL:
     L.rb_rs_free.argtypes = [p]
     L.rb_rs_free.restype = None
     L.rb_bounds_lookup.argtypes = [p, p, p, p, i64, p, p, p]
+    L.rb_validate_full.argtypes = [p, C.POINTER(Polygons), p, p, p, i32, d, d, d, p, i32, i64, d, p,
+                                   C.POINTER(d), p]
     L.rb_lps_from_arrays.argtypes = [C.POINTER(Grid), i64, p, p, p, i32, p, C.POINTER(p)]
     L.rb_rs_from_arrays.argtypes = [p, i32, i32, i64, p, p, p, p, C.POINTER(p)]
     L.rb_join_pointindex.argtypes = [p, p, i64, p, p, p, p, i32, i32, p, p, p]

@@ -142,4 +142,87 @@ def validate(index: ApproxIndex, xy, epsilon: float, max_points: int | None = 20
     return ValidationReport(n, len({k for k, _ in mism}), len(mism), len(fp), len(fn), maxd, float(epsilon))
 
 
-__all__ = ["validate", "ValidationReport"]
+def _bucket_grid(packed: PackedRegions, epsilon: float, extent_hint):
+    """Uniform grid of polygon MBRs expanded by epsilon (CSR), for rb_validate_full."""
+    npoly = packed.n_polygons
+    vstart = packed.ring_off[packed.poly_ring_off[:-1]]
+    vend = packed.ring_off[packed.poly_ring_off[1:]]
+    mnx = np.minimum.reduceat(packed.vx, vstart)
+    mxx = np.maximum.reduceat(packed.vx, vstart)
+    mny = np.minimum.reduceat(packed.vy, vstart)
+    mxy = np.maximum.reduceat(packed.vy, vstart)
+    del vend
+    x0, y0, ext = extent_hint
+    nb = int(min(1024, max(1, np.sqrt(4 * npoly))))
+    bs = max(ext / nb, 1e-300)
+    pad = 2.0 * epsilon
+    bx0 = np.clip(np.floor((mnx - pad - x0) / bs), 0, nb - 1).astype(np.int64)
+    bx1 = np.clip(np.floor((mxx + pad - x0) / bs), 0, nb - 1).astype(np.int64)
+    by0 = np.clip(np.floor((mny - pad - y0) / bs), 0, nb - 1).astype(np.int64)
+    by1 = np.clip(np.floor((mxy + pad - y0) / bs), 0, nb - 1).astype(np.int64)
+    counts = np.zeros(nb * nb + 1, np.int64)
+    pairs_b, pairs_p = [], []
+    for p in range(npoly):
+        ys = np.arange(by0[p], by1[p] + 1)
+        xs = np.arange(bx0[p], bx1[p] + 1)
+        b = (ys[:, None] * nb + xs[None, :]).ravel()
+        pairs_b.append(b)
+        pairs_p.append(np.full(len(b), p, np.int32))
+    pb = np.concatenate(pairs_b)
+    pp = np.concatenate(pairs_p)
+    o = np.argsort(pb, kind="stable")
+    pb, pp = pb[o], pp[o]
+    off = np.searchsorted(pb, np.arange(nb * nb + 1)).astype(np.int32)
+    mbr = np.stack([mnx, mny, mxx, mxy], 1).astype(np.float64)
+    return mbr, off, pp.astype(np.int32), nb, x0, y0, bs
+
+
+@dataclass
+class FullValidationReport:
+    """Every point checked (not a sample)."""
+    points: int
+    mismatched_points: int
+    false_positives: int
+    false_negatives: int
+    violations: int
+    owner_set_overflows: int
+    max_mismatch_distance: float
+    epsilon: float
+
+    @property
+    def ok(self) -> bool:
+        return self.violations == 0 and self.owner_set_overflows == 0
+
+    @property
+    def mismatch_fraction(self) -> float:
+        return self.mismatched_points / max(self.points, 1)
+
+    def as_dict(self) -> dict:
+        d = dict(self.__dict__)
+        d.update(ok=self.ok, mismatch_fraction=self.mismatch_fraction)
+        return d
+
+
+def validate_full(index: ApproxIndex, xy, epsilon: float) -> FullValidationReport:
+    """The complete validator (rb_validate_full): every point's approximate
+    owner regions against its exact owner regions; every mismatch must lie
+    within epsilon of the region's boundary."""
+    torch = N.require_cuda()
+    packed = index.packed
+    g = index.grid
+    mbr, off, bp, nb, bx0, by0, bs = _bucket_grid(packed, epsilon, (g.origin.x, g.origin.y, g.extent))
+    dev = DevicePolygons(packed)
+    t_mbr = torch.as_tensor(mbr).cuda()
+    t_off = torch.as_tensor(off).cuda()
+    t_bp = torch.as_tensor(bp if len(bp) else np.zeros(1, np.int32)).cuda()
+    t_xy, dt = index._xy(xy)
+    out = (C.c_int64 * 6)()
+    md = C.c_double()
+    N.check(N.load().rb_validate_full(index._h, C.byref(dev.desc), t_mbr.data_ptr(), t_off.data_ptr(),
+                                      t_bp.data_ptr(), nb, bx0, by0, bs, t_xy.data_ptr(), dt, int(t_xy.shape[0]),
+                                      float(epsilon), out, C.byref(md), N.stream_ptr()), "validate_full")
+    return FullValidationReport(int(out[0]), int(out[1]), int(out[2]), int(out[3]), int(out[4]), int(out[5]),
+                                float(md.value), float(epsilon))
+
+
+__all__ = ["validate", "ValidationReport", "validate_full", "FullValidationReport"]

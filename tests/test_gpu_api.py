@@ -221,3 +221,40 @@ def test_epsilon_validator(mode):
     assert rep.mismatched_points > 0  # the approximation is genuinely approximate
     if mode == 0:
         assert rep.false_negatives == 0
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_full_validator_matches_sampled(mode):
+    """rb_validate_full (every point, one kernel) agrees with the pairwise
+    validator on the same points: same mismatches, same max distance."""
+    from paper_2010_12548_b200 import workloads as W
+    from paper_2010_12548_b200.engine import ApproxIndex
+    from paper_2010_12548_b200.geometry import pack_regions
+    from paper_2010_12548_b200.grid import level_for_bound
+    from paper_2010_12548_b200.validate import validate, validate_full
+
+    w = W.c2(n=200_000, eps=10.0)
+    g = w.grid.with_level(level_for_bound(w.grid, w.epsilon))
+    idx = ApproxIndex(pack_regions(w.regions), g, mode)
+    a = validate(idx, w.xy, w.epsilon, max_points=None)
+    b = validate_full(idx, w.xy, w.epsilon)
+    assert b.ok and b.owner_set_overflows == 0, b.as_dict()
+    assert b.points == a.points
+    assert (b.mismatched_points, b.false_positives, b.false_negatives) == \
+        (a.mismatched_points, a.false_positives, a.false_negatives)
+    assert b.max_mismatch_distance == pytest.approx(a.max_mismatch_distance, rel=1e-12)
+    if mode == 0:
+        assert b.false_negatives == 0
+
+
+def test_full_validator_detects_violation():
+    """A coarse index (cells far larger than eps) must be reported."""
+    from paper_2010_12548_b200 import workloads as W
+    from paper_2010_12548_b200.engine import ApproxIndex
+    from paper_2010_12548_b200.geometry import pack_regions
+    from paper_2010_12548_b200.validate import validate_full
+
+    w = W.c2(n=100_000, eps=10.0)
+    idx = ApproxIndex(pack_regions(w.regions), w.grid.with_level(4), 1)
+    b = validate_full(idx, w.xy, w.epsilon)
+    assert b.violations > 0 and not b.ok
