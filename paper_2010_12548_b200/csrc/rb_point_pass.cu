@@ -86,7 +86,7 @@ struct PassArgs {
   int n_hot;
   int hcopies;  // warp kernel: copies of the shared histogram (lane & (hcopies-1) picks one)
   int hstride;  // warp kernel: words per histogram copy (== 1 mod 32: a bin's copies sit in distinct banks)
-  int ablate;   // timing experiments only (RB_ABLATE): 1 skip rare path, 2 skip node level, 4 skip root
+  int ablate;   // timing experiments only (RB_ABLATE): 1 skip the rare path
   int fold;     // ring kernel: cap on the drain period in warp-tiles (RB_FOLD, tests); 0 = automatic
 };
 
@@ -917,9 +917,12 @@ __device__ __forceinline__ void reds(uint32_t addr, uint32_t v) {
   asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
 
-// Rare path of the warp kernel: every owner of value v (boundary owner, owner
-// list) or an attribute outside the fixed-point window.  bins: shared address
-// of bin 0 (stride 12 bytes with an attribute, 4 without).
+// Rare path of the ring kernel: every owner of value v (owner list) or an
+// attribute outside the fixed-point window.  bins: shared address of bin 0
+// (stride 12 bytes with an attribute, 4 without).  The ring kernel's bins are
+// (region << 1) | boundary: interior-leaf and boundary-leaf points of a region
+// (k_reduce_fixed turns them into alpha = both, beta = boundary), so every
+// owner entry adds to exactly one bin.
 template <bool ATTR>
 __device__ __forceinline__ void add_owners_w(uint32_t bins, double* slow, const uint32_t* __restrict__ pool, uint32_t v,
                                           float w, int32_t qv, bool fast) {
@@ -931,16 +934,14 @@ __device__ __forceinline__ void add_owners_w(uint32_t bins, double* slow, const 
   } else {
     e = (v & RB_CODE_MASK) - 1u;  // (region << 1) | boundary
   }
+#pragma unroll 1
   for (uint32_t i = 0; i < n; ++i) {
     if (Lp) e = __ldg(Lp + 1 + i) & RB_CODE_MASK;
-    const uint32_t q = e & ~1u;
-    for (uint32_t b = q; b <= (q | (e & 1u)); ++b) {  // alpha bin, and beta when boundary
-      const uint32_t ad = bins + b * (ATTR ? 12u : 4u);
-      reds(ad, 1u);
-      if (ATTR) {
-        if (fast) { reds(ad + 4, (uint32_t)qv & 0xffffu); reds(ad + 8, (uint32_t)(qv >> 16)); }
-        else atomicAdd(&slow[b], (double)w);
-      }
+    const uint32_t ad = bins + e * (ATTR ? 12u : 4u);
+    reds(ad, 1u);
+    if (ATTR) {
+      if (fast) { reds(ad + 4, (uint32_t)qv & 0xffffu); reds(ad + 8, (uint32_t)(qv >> 16)); }
+      else atomicAdd(&slow[e], (double)w);
     }
   }
 }
@@ -1035,8 +1036,16 @@ __global__ void __launch_bounds__(NW * 32 + 32, NW <= 8 ? 2 : 1) k_point_pass_ri
     __shared__ float smax[NW];
     float mx = 0.f;
     const int64_t stride = a.n / 4096 > 0 ? a.n / 4096 : 1;
-    for (int64_t q = tid; q < 4096 && q * stride < a.n; q += NW * 32) {
-      const float v = fabsf(__ldg(a.attr + q * stride));
+    constexpr int NSAMP = (4096 + NW * 32 - 1) / (NW * 32);
+    float sv[NSAMP];
+#pragma unroll
+    for (int j = 0; j < NSAMP; ++j) {  // all loads in flight at once (one DRAM latency, not NSAMP)
+      const int64_t q = tid + (int64_t)j * NW * 32;
+      sv[j] = (q < 4096 && q * stride < a.n) ? __ldg(a.attr + q * stride) : 0.f;
+    }
+#pragma unroll
+    for (int j = 0; j < NSAMP; ++j) {
+      const float v = fabsf(sv[j]);
       if (isfinite(v)) mx = fmaxf(mx, v);
     }
     for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -1066,7 +1075,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, NW <= 8 ? 2 : 1) k_point_pass_ri
   // the single node level is the leaf level (k = L - T0), addressable with 32-bit offsets
   const bool onelevel = nlev == 1 && a.V.ks[0] == s0 && a.V.nodes0_len < (int64_t(1) << 32);
   const uint32_t bins = smem_u32(h3) + (uint32_t)((lane & (C - 1)) * P) * 4u;  // this lane's copy
-  const uint32_t h3s = bins - BS;  // interior owner value v = 2*region + 1 -> bin 2*region at h3s + v * BS
+  const uint32_t h3s = bins - BS;  // single owner v: code (v & CODE_MASK) = ((region << 1) | boundary) + 1 -> bin code-1
   const uint32_t dms = smem_u32(dummy) + lane * BS;
   // ---- software pipeline over this CTA's tiles (k = 0, 1, ...); iteration k runs
   //   C(k-2): accumulate the owner values nv[] loaded during iteration k-1
@@ -1105,8 +1114,9 @@ __global__ void __launch_bounds__(NW * 32 + 32, NW <= 8 ? 2 : 1) k_point_pass_ri
           qv = __float2int_rn(w2[j] * sc);
           fast = ((__float_as_uint(w2[j]) & 0x7fffffffu) - wminb) < wspan;
         }
-        // interior single owner (odd code, no list) with an in-window attribute
-        const bool common = ((v & (RB_VALUE_LIST | 1u)) == 1u) & fast;
+        // single owner (no list), interior or boundary leaf, with an in-window attribute
+        // (v == 0, no owner, lands on bin -1: the dummy slot before copy 0, or >= 3 pad words of the copy before)
+        const bool common = ((v & RB_VALUE_LIST) == 0u) & fast;
         // unconditional REDs (a predicated RED becomes a branch): off-path points hit this lane's dummy bin
         const uint32_t ad = common ? h3s + (v & RB_CODE_MASK) * BS : dms;
         reds(ad, 1u);
@@ -1123,7 +1133,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, NW <= 8 ? 2 : 1) k_point_pass_ri
         for (int j = 0; j < PPT; ++j) {
           const uint32_t v = nv[j];
           const bool fast = !ATTR || (((__float_as_uint(w2[j]) & 0x7fffffffu) - wminb) < wspan);
-          const bool rare = !(((v & (RB_VALUE_LIST | 1u)) == 1u) & fast) & (v != 0u);
+          const bool rare = (((v & RB_VALUE_LIST) != 0u) | !fast) & (v != 0u);
           const uint32_t mk = __ballot_sync(0xffffffffu, rare);
           if (mk) {
             if (rare) rq[(qh + qn + __popc(mk & ((1u << lane) - 1u))) & 63] = make_uint2(v, __float_as_uint(w2[j]));
@@ -1158,7 +1168,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, NW <= 8 ? 2 : 1) k_point_pass_ri
       uint32_t anyn = 0;
 #pragma unroll
       for (int j = 0; j < PPT; ++j) anyn |= rv[j];
-      if (!(a.ablate & 2) && __any_sync(0xffffffffu, (int32_t)anyn < 0)) {  // RB_VALUE_NODE = bit 31
+      if (__any_sync(0xffffffffu, (int32_t)anyn < 0)) {  // RB_VALUE_NODE = bit 31
         if (onelevel) {  // one node level = the leaf cells of a root cell, row-major (32-bit offsets)
 #pragma unroll
           for (int j = 0; j < PPT; ++j) {
@@ -1257,7 +1267,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, NW <= 8 ? 2 : 1) k_point_pass_ri
 #pragma unroll
       for (int j = 0; j < PPT; ++j) {
         const uint32_t* rp = root + (((by[j] >> s0) << T0) | (bx[j] >> s0));
-        rv[j] = ldg_pred(rp, sv[j] == 0xffffu && !(a.ablate & 4), sv[j]);
+        rv[j] = ldg_pred(rp, sv[j] == 0xffffu, sv[j]);
       }
     }
   }
@@ -1323,7 +1333,8 @@ __global__ void k_attr_scale(const float* attr, int64_t n, int* scale_exp) {
 // and are combined in fixed warp order.
 __global__ void __launch_bounds__(1024) k_reduce_fixed(const uint32_t* part_cnt, const long long* part_acc,
                                                        const double* part_sum, int nrows, int R2, bool attr,
-                                                       const int* scale_exp, int64_t* cnt_out, double* sum_out) {
+                                                       bool ib, const int* scale_exp, int64_t* cnt_out,
+                                                       double* sum_out) {
   __shared__ unsigned long long sc[32][32];
   __shared__ long long sa[32][32];
   __shared__ double ss[32][32];
@@ -1342,8 +1353,16 @@ __global__ void __launch_bounds__(1024) k_reduce_fixed(const uint32_t* part_cnt,
   sa[warp][lane] = f;
   ss[warp][lane] = s;
   __syncthreads();
-  if (warp == 0 && q < R2) {
+  if (warp == 0) {
     for (int w2 = 1; w2 < 32; ++w2) { c += sc[w2][lane]; f += sa[w2][lane]; s += ss[w2][lane]; }
+    if (ib) {  // ring kernel bins: 2r = interior-leaf points, 2r+1 = boundary-leaf points -> alpha = both
+      const unsigned long long c1 = __shfl_down_sync(0xffffffffu, c, 1);
+      const long long f1 = __shfl_down_sync(0xffffffffu, f, 1);
+      const double s1 = __shfl_down_sync(0xffffffffu, s, 1);
+      if ((lane & 1) == 0) { c += c1; f += f1; s += s1; }
+    }
+  }
+  if (warp == 0 && q < R2) {
     cnt_out[q] += (int64_t)c;
     if (attr) sum_out[q] += ldexp((double)f, -*scale_exp) + s;
   }
@@ -1588,7 +1607,7 @@ int point_pass(const rb_approx* A, const void* xy, int32_t dtype, int64_t n, con
       if (env_ci >= 0 && c != env_ci) continue;
       const WarpCfg& W = kWarpCfgs[c];
       const int wpb = attr ? 3 : 1;
-      const int P = R2 * wpb + (int)((33 - (R2 * wpb) % 32) % 32);  // P % 32 == 1
+      const int P = R2 * wpb + 3 + (int)((33 - (R2 * wpb + 3) % 32) % 32);  // P % 32 == 1, >= 3 pad words
       for (int C = attr ? 8 : 1; C >= 1; C >>= 1) {
         if (env_copies > 0 && C > env_copies) continue;
         const size_t bins_w = (size_t)W.nw * 512 + 32 * (attr ? 12 : 4) + ((((size_t)C * P * 4) + 15) & ~(size_t)15) +
@@ -1633,7 +1652,7 @@ int point_pass(const rb_approx* A, const void* xy, int32_t dtype, int64_t n, con
     if (e) return cuda_fail(e, "k_point_pass_ring");
     if (tstop()) return RB_CUDA_ERROR;
     k_reduce_fixed<<<std::max(1, (R2 + 31) / 32), 1024, 0, s>>>(a.part_cnt, a.part_acc, a.part_sum, blocks, R2,
-                                                                attr != nullptr, scale, cnt_out, sum_out);
+                                                                attr != nullptr, true, scale, cnt_out, sum_out);
     RB_CUDA(cudaGetLastError());
     ++g_launches;
     RB_CUDA(cudaFreeAsync(scratch, s));
@@ -1669,7 +1688,7 @@ int point_pass(const rb_approx* A, const void* xy, int32_t dtype, int64_t n, con
   if (tstop()) return RB_CUDA_ERROR;
   if (smem_hist) {
     k_reduce_fixed<<<std::max(1, (R2 + 31) / 32), 1024, 0, s>>>(a.part_cnt, a.part_acc, a.part_sum, blocks, R2,
-                                                                attr != nullptr, scale, cnt_out, sum_out);
+                                                                attr != nullptr, false, scale, cnt_out, sum_out);
     RB_CUDA(cudaGetLastError());
     ++g_launches;
   }

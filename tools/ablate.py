@@ -1,4 +1,5 @@
-"""Point-pass ablations on the GPU (timing only): which part of the pass costs what.
+"""Point-pass ablations on the GPU (timing only): which part of the pass costs what
+(RB_ABLATE=1 skips the rare path; RASTERBOUND_B200_LIB picks a library build for A/B).
   c2 SUM / c2 COUNT          the real workload
   square SUM / square COUNT  one square region over the whole domain: every point resolves
                              from the shared-memory summary (no L2 index traffic)
