@@ -1424,6 +1424,10 @@ static cudaError_t launch_smem(const PassArgs& a, size_t smem, cudaStream_t s, i
   if (cached_blocks < 0 || cached_smem != smem) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, RB_SMEM_BUDGET);
     if (e) return e;
+    if (const char* cv = getenv("RB_CARVEOUT")) {  // experiments: shared-memory share of the L1 (percent)
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(cv));
+      if (e) return e;
+    }
     int per_sm = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem);
     if (e) return e;
@@ -1443,6 +1447,10 @@ static cudaError_t tma_blocks(size_t smem, int* blocks_out) {
   if (cached_blocks < 0 || cached_smem != smem) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, RB_SMEM_BUDGET);
     if (e) return e;
+    if (const char* cv = getenv("RB_CARVEOUT")) {  // experiments: shared-memory share of the L1 (percent)
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(cv));
+      if (e) return e;
+    }
     int per_sm = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, RB_CONS + 32, smem);
     if (e) return e;
@@ -1467,7 +1475,13 @@ static cudaError_t run_smem(const PassArgs& a, int blocks, size_t smem, cudaStre
 
 // per-warp-ring kernel configurations (consumer warps, points per lane, stages)
 struct WarpCfg { int nw, ppt, nst; };
-static const WarpCfg kWarpCfgs[] = {{16, 4, 4}, {16, 4, 3}, {15, 4, 2}, {16, 2, 6}};
+// Preference order.  Shared memory and the L1 data cache share 256 KB per SM, and the carveout is the
+// smallest step (..., 164, 196, 228 KB) that holds the CTA's shared memory: the root / node lookups hit
+// in the L1 that is left.  A 3-stage ring with <= 4 histogram copies (~190 KB for C2 SUM -> 60 KB of
+// L1) beat the 4-stage ring (~220 KB -> 28 KB of L1): 0.475 -> 0.444 ms; forcing the 3-stage ring to a
+// 228 KB carveout gave 0.469 ms.  2 points per lane (0.54 ms), 3 points per lane (0.48 ms) and 2-stage
+// rings (0.47 ms) were slower (profiles/round1/ring_config_sweep.txt).
+static const WarpCfg kWarpCfgs[] = {{16, 4, 3}, {16, 4, 4}, {16, 4, 2}, {15, 4, 2}};
 
 template <int XY, bool ATTR, int NW, int PPT, int NST>
 static cudaError_t warp_run(const PassArgs& a, size_t smem, cudaStream_t s, int* blocks, bool launch) {
@@ -1477,6 +1491,10 @@ static cudaError_t warp_run(const PassArgs& a, size_t smem, cudaStream_t s, int*
   if (cached_blocks < 0 || cached_smem != smem) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, RB_SMEM_BUDGET);
     if (e) return e;
+    if (const char* cv = getenv("RB_CARVEOUT")) {  // experiments: shared-memory share of the L1 (percent)
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(cv));
+      if (e) return e;
+    }
     int per_sm = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NW * 32 + 32, smem);
     if (e) return e;
@@ -1492,10 +1510,10 @@ static cudaError_t warp_run(const PassArgs& a, size_t smem, cudaStream_t s, int*
 template <int XY, bool ATTR>
 static cudaError_t warp_dispatch(int ci, const PassArgs& a, size_t smem, cudaStream_t s, int* blocks, bool launch) {
   switch (ci) {
-    case 0: return warp_run<XY, ATTR, 16, 4, 4>(a, smem, s, blocks, launch);
-    case 1: return warp_run<XY, ATTR, 16, 4, 3>(a, smem, s, blocks, launch);
-    case 2: return warp_run<XY, ATTR, 15, 4, 2>(a, smem, s, blocks, launch);
-    default: return warp_run<XY, ATTR, 16, 2, 6>(a, smem, s, blocks, launch);
+    case 0: return warp_run<XY, ATTR, 16, 4, 3>(a, smem, s, blocks, launch);
+    case 1: return warp_run<XY, ATTR, 16, 4, 4>(a, smem, s, blocks, launch);
+    case 2: return warp_run<XY, ATTR, 16, 4, 2>(a, smem, s, blocks, launch);
+    default: return warp_run<XY, ATTR, 15, 4, 2>(a, smem, s, blocks, launch);
   }
 }
 
@@ -1601,15 +1619,15 @@ int point_pass(const rb_approx* A, const void* xy, int32_t dtype, int64_t n, con
     }
     const size_t summ_w = A->S >= 0 ? ((size_t)2 << (2 * A->S)) : 16;
     const int ncfg = (int)(sizeof(kWarpCfgs) / sizeof(kWarpCfgs[0]));
-    // histogram copies: up to 8 with an attribute (distinct-value REDs to one word serialise;
-    // same-address count increments are aggregated by the hardware), 1 for COUNT
+    // histogram copies: up to 4 with an attribute (distinct-value REDs to one word serialise;
+    // same-address count increments are aggregated by the hardware), 1 for COUNT; 8 copies cost
+    // more L1 (carveout) than they save in RED conflicts
     for (int c = 0; c < ncfg && wci < 0; ++c) {
       if (env_ci >= 0 && c != env_ci) continue;
       const WarpCfg& W = kWarpCfgs[c];
       const int wpb = attr ? 3 : 1;
       const int P = R2 * wpb + 3 + (int)((33 - (R2 * wpb + 3) % 32) % 32);  // P % 32 == 1, >= 3 pad words
-      for (int C = attr ? 8 : 1; C >= 1; C >>= 1) {
-        if (env_copies > 0 && C > env_copies) continue;
+      for (int C = env_copies > 0 ? env_copies : (attr ? 4 : 1); C >= 1; C >>= 1) {
         const size_t bins_w = (size_t)W.nw * 512 + 32 * (attr ? 12 : 4) + ((((size_t)C * P * 4) + 15) & ~(size_t)15) +
                               (attr ? (size_t)R2 * 8 : 0);
         const size_t need = (size_t)W.nw * W.nst * W.ppt * 32 * pt_bytes + bins_w + summ_w;
