@@ -804,7 +804,18 @@ static int index_impl(int L, int64_t total_cells, const int32_t* cp_in, const ui
     // up to L = 16 (C2: 0.503 -> 0.487 ms over T0 = 10); deeper grids keep an 8 MB root (C4)
     T0 = opts->root_level >= 0 ? std::min(opts->root_level, L) : (L <= 16 ? std::min(L, 12) : 11);
     int rem = L - T0;
-    if (rem > 0) {
+    if (const char* e = getenv("RB_NODE_KS")) {  // experiments: explicit node split, e.g. "2,5"
+      for (const char* c = e; *c;) {
+        const int v = atoi(c);
+        if (v <= 0 || v > rem) { ks.clear(); break; }
+        ks.push_back(v);
+        rem -= v;
+        while (*c && *c != ',') ++c;
+        if (*c == ',') ++c;
+      }
+      if (rem != 0) return fail(RB_CONFIG_ERROR, "RB_NODE_KS must split L - root_level exactly");
+    }
+    if (ks.empty() && rem > 0) {
       int first = rem % k ? rem % k : k;
       ks.push_back(first);
       rem -= first;

@@ -1301,6 +1301,423 @@ __global__ void __launch_bounds__(NW * 32 + 32, NW <= 8 ? 2 : 1) k_point_pass_ri
   }
 }
 
+// ---------------------------------------------------------------------------
+// Deep-index variant of the ring kernel (C4 class: a region set beyond shared
+// memory and two or more node levels below the root, L <= 20, L - T0 <= 16).
+//
+// The same producer warp + 16 consumer warps and TMA ring, with the node
+// descent spread over the software pipeline so that every dependent index load
+// is consumed one iteration after it is issued:
+//   C(k-3): accumulate the owner values nv2[] of tile k-3
+//   B2(k-2): node levels 1.. of tile k-2 from nv1[] -> nv2[]
+//   B1(k-1): node level 0 of tile k-1 from its root values rv[] -> nv1[]
+//   A(k):   tile k: ring -> quantise -> summary -> root loads -> rv[]
+// Only the low L - T0 bits of a point's cell coordinates address its node
+// slots, so a tile in flight carries them packed in one register per point.
+//
+// Accumulation keeps the global-histogram semantics of
+// k_point_pass_tma: interior single owners of a hot region (rb_approx_set_hot,
+// value bits 18..29 = slot + 1) with an in-window attribute take three shared
+// REDs into the region's privatised alpha slot; every other owner entry (cold
+// region, boundary leaf -> alpha and beta, owner list, out-of-window
+// attribute) goes through the per-warp rare queue to global REDG (u64 count,
+// f64 sum).  Hot slots drain to the CTA's fixed-point row like the ring
+// kernel's bins and are flushed into the global outputs at the end.
+// ---------------------------------------------------------------------------
+template <bool ATTR>
+__device__ __forceinline__ void add_owners_g(uint32_t bins, const uint32_t* __restrict__ pool, uint32_t v, float w,
+                                             int32_t qv, bool fast, unsigned long long* gcnt, double* gsum) {
+  uint32_t n = 1, x = v;
+  const uint32_t* Lp = nullptr;
+  if (v & RB_VALUE_LIST) {
+    Lp = pool + (v & RB_VALUE_PAYLOAD);
+    n = __ldg(Lp) & ~RB_POOL_COUNT_FLAG;
+  } else {
+    x = ((v & RB_CODE_MASK) - 1u) | (v & (RB_HOT_BITS << RB_HOT_SHIFT));  // (region << 1) | boundary, hot slot
+  }
+#pragma unroll 1
+  for (uint32_t i = 0; i < n; ++i) {
+    if (Lp) {
+      const uint32_t y = __ldg(Lp + 1 + i);
+      x = (y & RB_CODE_MASK) | (y & (RB_HOT_BITS << RB_HOT_SHIFT));
+    }
+    const uint32_t e = x & RB_CODE_MASK, q = e & ~1u, slot = (x >> RB_HOT_SHIFT) & RB_HOT_BITS;
+    if (slot && !(e & 1u) && fast) {  // privatised alpha slot
+      const uint32_t ad = bins + (slot - 1u) * (ATTR ? 12u : 4u);
+      reds(ad, 1u);
+      if (ATTR) { reds(ad + 4, (uint32_t)qv & 0xffffu); reds(ad + 8, (uint32_t)(qv >> 16)); }
+      continue;
+    }
+    atomicAdd(&gcnt[q], 1ull);
+    if (ATTR) atomicAdd(&gsum[q], (double)w);
+    if (e & 1u) {  // boundary leaf: beta as well
+      atomicAdd(&gcnt[q + 1], 1ull);
+      if (ATTR) atomicAdd(&gsum[q + 1], (double)w);
+    }
+  }
+}
+
+// predicated global REDs (a C++ `if` around an atomic compiles to a branch per point)
+__device__ __forceinline__ void redg_count(unsigned long long* p, bool pred) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %1, 0;\n @q red.global.add.u64 [%0], 1;\n}\n" ::"l"(p),
+               "r"((uint32_t)pred)
+               : "memory");
+}
+__device__ __forceinline__ void redg_sum(double* p, double w, bool pred) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %1, 0;\n @q red.global.add.f64 [%0], %2;\n}\n" ::"l"(p),
+               "r"((uint32_t)pred), "d"(w)
+               : "memory");
+}
+
+template <int XY, bool ATTR, int NW, int PPT, int NST>
+__global__ void __launch_bounds__(NW * 32 + 32, 1) k_point_pass_deep(PassArgs a) {
+  constexpr int PB = XY == 0 ? 16 : 8;
+  constexpr int WT = PPT * 32;
+  constexpr int TP = NW * WT;
+  constexpr uint32_t XYB = TP * PB, ATB = ATTR ? TP * 4 : 0, STAGE = XYB + ATB;
+  constexpr uint32_t BS = ATTR ? 12u : 4u;
+  const int C = a.hcopies, P = a.hstride, NH = a.n_hot;
+  // Drains are partitioned: warp w drains hot slots q with (q / 32) % NW == w every FOLD of its own tiles.
+  // Warps stay within NST tiles of each other (one ring), so between two drains of a copy-slot every
+  // warp adds at most (FOLD + NST) * WT / C values to it: <= NW * 30 * WT (61440 for NW = 16, WT = 128)
+  // plus <= 63 queued per warp, which keeps the low halves below 2^32 and the high halves within 2^30.
+  int FOLD = C * (61440 / (NW * WT) > 0 ? 61440 / (NW * WT) : 1) - NST;
+  if (FOLD < 1) FOLD = 1;
+  if (a.fold > 0 && a.fold < FOLD) FOLD = a.fold;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t full[NST], empty[NST];
+  __shared__ float smax[NW];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // layout: [NST stages][per-warp rare queues: NW x 64 x 8 B][32 dummy bins][C hot-slot copies of P words][summary u16]
+  uint2* rq = (uint2*)(smem + (size_t)NST * STAGE) + (size_t)(warp < NW ? warp : 0) * 64;
+  unsigned char* dummy = smem + (size_t)NST * STAGE + NW * 64 * 8;
+  uint32_t* h3 = (uint32_t*)(dummy + 32 * BS);
+  const size_t h3b = (((size_t)C * P * 4) + 15) & ~(size_t)15;
+  uint16_t* summ = (uint16_t*)((unsigned char*)h3 + h3b);
+  long long* prow = a.part_acc + (size_t)blockIdx.x * (NH > 0 ? NH : 1);
+  const bool has_summ = a.V.S >= 0;
+  const int S = has_summ ? a.V.S : 0;
+  constexpr int NT = NW * 32 + 32;
+  for (int q = tid; q < C * P; q += NT) h3[q] = 0;
+  if (ATTR)
+    for (int q = tid; q < NH; q += NT) prow[q] = 0;
+  if (has_summ) {
+    const int nsum = 1 << (2 * S);
+    const uint4* src = (const uint4*)a.V.summary;
+    for (int q = tid; q < (nsum >> 3); q += NT) ((uint4*)summ)[q] = __ldg(src + q);
+    for (int q = (nsum & ~7) + tid; q < nsum; q += NT) summ[q] = a.V.summary[q];
+  }
+  if (tid == 0) {
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  const int64_t nmain = a.n & ~(int64_t)3;
+  const int64_t ntiles = (nmain + TP - 1) / TP;
+  const int64_t G = gridDim.x;
+  if (warp == NW) {  // producer
+    if (lane == 0) {
+      uint64_t pol;
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+      int st = 0;
+      uint32_t ph = 0;
+      int64_t k = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += G, ++k) {
+        if (k >= NST) mbar_wait(&empty[st], ph ^ 1u);
+        const int64_t p0 = t * TP;
+        const uint32_t m = (uint32_t)(p0 + TP <= nmain ? TP : nmain - p0);
+        unsigned char* dst = smem + (size_t)st * STAGE;
+        mbar_expect_tx(&full[st], m * (PB + (ATTR ? 4 : 0)));
+        bulk_g2s(dst, (const char*)a.xy + p0 * PB, m * PB, &full[st], pol);
+        if (ATTR) bulk_g2s(dst + XYB, a.attr + p0, m * 4, &full[st], pol);
+        if (++st == NST) { st = 0; ph ^= 1u; }
+      }
+    }
+    return;
+  }
+  // consumers: fixed-point scale from the same strided sample as every other CTA
+  float sc = 1.f;
+  uint32_t wminb = 0, wspan = 0;
+  int Sx = 0;
+  if (ATTR) {
+    float mx = 0.f;
+    const int64_t stride = a.n / 4096 > 0 ? a.n / 4096 : 1;
+    constexpr int NSAMP = (4096 + NW * 32 - 1) / (NW * 32);
+    float sv[NSAMP];
+#pragma unroll
+    for (int j = 0; j < NSAMP; ++j) {
+      const int64_t q = tid + (int64_t)j * NW * 32;
+      sv[j] = (q < 4096 && q * stride < a.n) ? __ldg(a.attr + q * stride) : 0.f;
+    }
+#pragma unroll
+    for (int j = 0; j < NSAMP; ++j) {
+      const float v = fabsf(sv[j]);
+      if (isfinite(v)) mx = fmaxf(mx, v);
+    }
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) smax[warp] = mx;
+    asm volatile("bar.sync 1, %0;" ::"r"(NW * 32) : "memory");
+    mx = 0.f;
+    for (int w2 = 0; w2 < NW; ++w2) mx = fmaxf(mx, smax[w2]);
+    if (mx > 0.f) {
+      int e = 0;
+      frexpf(mx, &e);
+      Sx = 29 - e;
+    }
+    Sx = Sx < -96 ? -96 : (Sx > 126 ? 126 : Sx);
+    sc = __int_as_float((Sx + 127) << 23);
+    wminb = (uint32_t)((20 - Sx + 127) << 23);
+    wspan = (uint32_t)((30 - Sx + 127) << 23) - wminb;
+  }
+  const double ox = a.ox, oy = a.oy, inv_side = a.inv_side;
+  const uint32_t* __restrict__ root = a.V.root;
+  const uint32_t* __restrict__ pool = a.V.pool;
+  const uint32_t* __restrict__ nodes0 = a.V.nodes[0];
+  const uint32_t* __restrict__ nodes1 = a.V.nodes[a.V.nlev > 1 ? 1 : 0];
+  const int L = a.V.L, T0 = a.V.T0, s0 = L - T0, nlev = a.V.nlev, sS = L - S;
+  // node slots from the packed low coordinates c = (bx & m0) | (by & m0) << 16 (32-bit node offsets)
+  const int k0 = a.V.ks[0], s1 = s0 - k0, k1 = nlev > 1 ? a.V.ks[1] : 0, s2 = s1 - k1;
+  const uint32_t hibits = ~((1u << L) - 1u);
+  const uint32_t m0 = (1u << s0) - 1u, mk0 = (1u << k0) - 1u, mk1 = (1u << k1) - 1u;
+  const uint32_t bins = smem_u32(h3) + (uint32_t)((lane & (C - 1)) * P) * 4u;
+  const uint32_t h3s = bins - BS;  // hot field (slot + 1) -> slot bin at h3s + field * BS
+  const uint32_t dms = smem_u32(dummy) + lane * BS;
+  unsigned long long* gcnt = a.gcnt;
+  double* gsum = a.gsum;
+  int qh = 0, qn = 0;
+  auto rare_flush = [&](int nitems) {
+    if (lane < nitems) {
+      const uint2 it = rq[(qh + lane) & 63];
+      const float ww = __uint_as_float(it.y);
+      const bool fast = !ATTR || (((it.y & 0x7fffffffu) - wminb) < wspan);
+      add_owners_g<ATTR>(bins, pool, it.x, ww, ATTR ? __float2int_rn(ww * sc) : 0, fast, gcnt, gsum);
+    }
+    __syncwarp();
+  };
+  uint32_t rv[PPT], c1[PPT], c2[PPT], nv1[PPT], nv2[PPT];
+  float w1[PPT], w2[PPT], w3[PPT];
+#pragma unroll
+  for (int j = 0; j < PPT; ++j) { rv[j] = c1[j] = c2[j] = nv1[j] = nv2[j] = 0u; w1[j] = w2[j] = w3[j] = 0.f; }
+  int st = 0;
+  uint32_t ph = 0;
+  int dk = 0;
+  const int64_t K = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / G + 1 : 0;
+  for (int64_t k = 0; k < K + 3; ++k) {
+    // ------------------------------------------------------------ C(k-3)
+    if (k >= 3) {
+      bool anyrare = false;
+#pragma unroll
+      for (int j = 0; j < PPT; ++j) {
+        const uint32_t v = nv2[j];
+        int32_t qv = 0;
+        bool fast = true;
+        if (ATTR) {
+          qv = __float2int_rn(w3[j] * sc);
+          fast = ((__float_as_uint(w3[j]) & 0x7fffffffu) - wminb) < wspan;
+        }
+        const uint32_t hot = (v >> RB_HOT_SHIFT) & RB_HOT_BITS;
+        // interior single owner with an in-window attribute: a hot region's privatised slot, else
+        // predicated global REDs on its alpha bin; everything else takes the rare queue
+        const bool single = ((v & (RB_VALUE_LIST | 1u)) == 1u) & fast;
+        const bool common = single & (hot != 0u);
+        const uint32_t ad = common ? h3s + hot * BS : dms;
+        reds(ad, 1u);
+        if (ATTR) {
+          reds(ad + 4, (uint32_t)qv & 0xffffu);
+          reds(ad + 8, (uint32_t)(qv >> 16));
+        }
+        const bool cold = single & (hot == 0u);
+        const uint32_t q = (v & RB_CODE_MASK) - 1u;
+        redg_count(gcnt + q, cold);
+        if (ATTR) redg_sum(gsum + q, (double)w3[j], cold);
+        anyrare |= !single & (v != 0u);
+      }
+      if (__any_sync(0xffffffffu, anyrare)) {
+#pragma unroll
+        for (int j = 0; j < PPT; ++j) {
+          const uint32_t v = nv2[j];
+          const bool fast = !ATTR || (((__float_as_uint(w3[j]) & 0x7fffffffu) - wminb) < wspan);
+          const bool rare = !(((v & (RB_VALUE_LIST | 1u)) == 1u) & fast) & (v != 0u);
+          const uint32_t mk = __ballot_sync(0xffffffffu, rare);
+          if (mk) {
+            if (rare) rq[(qh + qn + __popc(mk & ((1u << lane) - 1u))) & 63] = make_uint2(v, __float_as_uint(w3[j]));
+            qn += __popc(mk);
+            if (qn >= 32) {
+              __syncwarp();
+              rare_flush(32);
+              qh = (qh + 32) & 63;
+              qn -= 32;
+            }
+          }
+        }
+      }
+      if (ATTR && ++dk == FOLD) {  // drain this warp's share of the hot slots into the CTA's row
+        dk = 0;
+        __syncwarp();
+        for (int q = warp * 32 + lane; q < NH; q += NW * 32) {
+          long long f = 0;
+          for (int c = 0; c < C; ++c) {
+            const uint32_t lo = atomicExch(&h3[c * P + 3 * q + 1], 0u);
+            const uint32_t hi = atomicExch(&h3[c * P + 3 * q + 2], 0u);
+            f += ((long long)(int32_t)hi << 16) + (long long)lo;
+          }
+          if (f) atomicAdd((unsigned long long*)&prow[q], (unsigned long long)f);
+        }
+      }
+    }
+    // ------------------------------------------------------------ B2(k-2): node levels 1..
+    if (k >= 2 && k <= K + 1) {
+#pragma unroll
+      for (int j = 0; j < PPT; ++j) { w3[j] = w2[j]; nv2[j] = nv1[j]; }
+      uint32_t anyn = 0;
+#pragma unroll
+      for (int j = 0; j < PPT; ++j) anyn |= nv2[j];
+      if (nlev > 1 && __any_sync(0xffffffffu, (int32_t)anyn < 0)) {
+#pragma unroll
+        for (int j = 0; j < PPT; ++j) {
+          const uint32_t slot = (((c2[j] >> (16 + s2)) & mk1) << k1) | ((c2[j] >> s2) & mk1);
+          const uint32_t off = ((nv2[j] & RB_VALUE_PAYLOAD) << (2 * k1)) | slot;
+          nv2[j] = ldg_pred(nodes1 + off, (int32_t)nv2[j] < 0, nv2[j]);
+        }
+        if (nlev > 2) {  // deeper trees: the remaining levels in place (one more dependent load each)
+          int s = s2;
+#pragma unroll 1
+          for (int li = 2; li < nlev; ++li) {
+            const int kk = a.V.ks[li];
+            const uint32_t* __restrict__ nodes = a.V.nodes[li];
+            s -= kk;
+            const uint32_t msk = (1u << kk) - 1u;
+#pragma unroll
+            for (int j = 0; j < PPT; ++j) {
+              const uint32_t slot = (((c2[j] >> (16 + s)) & msk) << kk) | ((c2[j] >> s) & msk);
+              const uint32_t off = ((nv2[j] & RB_VALUE_PAYLOAD) << (2 * kk)) | slot;
+              nv2[j] = ldg_pred(nodes + off, (int32_t)nv2[j] < 0, nv2[j]);
+            }
+          }
+        }
+      }
+    }
+    // ------------------------------------------------------------ B1(k-1): node level 0
+    if (k >= 1 && k <= K) {
+#pragma unroll
+      for (int j = 0; j < PPT; ++j) { w2[j] = w1[j]; c2[j] = c1[j]; }
+      uint32_t anyn = 0;
+#pragma unroll
+      for (int j = 0; j < PPT; ++j) anyn |= rv[j];
+      if (__any_sync(0xffffffffu, (int32_t)anyn < 0)) {
+#pragma unroll
+        for (int j = 0; j < PPT; ++j) {
+          const uint32_t slot = (((c1[j] >> (16 + s1)) & mk0) << k0) | ((c1[j] >> s1) & mk0);
+          const uint32_t off = ((rv[j] & RB_VALUE_PAYLOAD) << (2 * k0)) | slot;
+          nv1[j] = ldg_pred(nodes0 + off, (int32_t)rv[j] < 0, rv[j]);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < PPT; ++j) nv1[j] = rv[j];
+      }
+    }
+    // ------------------------------------------------------------ A(k)
+    if (k < K) {
+      const int64_t t = blockIdx.x + k * G;
+      mbar_wait_warp(&full[st], ph);
+      const unsigned char* tile = smem + (size_t)st * STAGE;
+      double x[PPT], y[PPT];
+#pragma unroll
+      for (int j = 0; j < PPT; ++j) {
+        const int pi = warp * WT + lane + 32 * j;
+        if (XY == 0) {
+          const double2 v2 = ((const double2*)tile)[pi];
+          x[j] = v2.x; y[j] = v2.y;
+        } else {
+          const float2 v2 = ((const float2*)tile)[pi];
+          x[j] = (double)v2.x; y[j] = (double)v2.y;
+        }
+        w1[j] = ATTR ? ((const float*)(tile + XYB))[pi] : 0.f;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+      if (++st == NST) { st = 0; ph ^= 1u; }
+      uint32_t bx[PPT], by[PPT];
+      bool anybad = false;
+#pragma unroll
+      for (int j = 0; j < PPT; ++j) {
+        const double tx = __fma_rn(__dsub_rn(x[j], ox), inv_side, 1048576.0);
+        const double ty = __fma_rn(__dsub_rn(y[j], oy), inv_side, 1048576.0);
+        bx[j] = (uint32_t)__double2hiint(tx) - 0x41300000u;
+        by[j] = (uint32_t)__double2hiint(ty) - 0x41300000u;
+        const uint32_t fx = (uint32_t)__double2loint(tx) + 8u, fy = (uint32_t)__double2loint(ty) + 8u;
+        anybad |= ((bx[j] | by[j]) & hibits) != 0u;
+        anybad |= (fx < 16u) | (fy < 16u);
+      }
+      const int64_t p0 = t * TP + warp * WT;
+      uint32_t killm = 0;
+      if (__any_sync(0xffffffffu, anybad) || p0 + WT > nmain) {
+        const int64_t mm = nmain - p0;
+        const int m = (int)(mm >= WT ? WT : (mm > 0 ? mm : 0));
+#pragma unroll
+        for (int j = 0; j < PPT; ++j) {
+          const double tx = __fma_rn(__dsub_rn(x[j], ox), inv_side, 1048576.0);
+          const double ty = __fma_rn(__dsub_rn(y[j], oy), inv_side, 1048576.0);
+          const uint32_t fx = (uint32_t)__double2loint(tx) + 8u, fy = (uint32_t)__double2loint(ty) + 8u;
+          const bool bad = (((bx[j] | by[j]) & hibits) != 0u) | (fx < 16u) | (fy < 16u);
+          if (lane + 32 * j >= m) {
+            bx[j] = 0; by[j] = 0; killm |= 1u << j;
+          } else if (bad) {
+            const uint64_t qq =
+                quantize_exact(a.xy, p0 + lane + 32 * j, XY, ox, oy, a.side, a.lim, a.first_bad, a.idx_base);
+            if (qq != ~0ull) { bx[j] = (uint32_t)qq; by[j] = (uint32_t)(qq >> 32); }
+            else { bx[j] = 0; by[j] = 0; killm |= 1u << j; }
+          }
+        }
+      }
+      uint32_t sv[PPT];
+#pragma unroll
+      for (int j = 0; j < PPT; ++j) sv[j] = has_summ ? (uint32_t)summ[((by[j] >> sS) << S) | (bx[j] >> sS)] : 0xffffu;
+      if (killm) {
+#pragma unroll
+        for (int j = 0; j < PPT; ++j)
+          if (killm & (1u << j)) sv[j] = 0u;
+      }
+#pragma unroll
+      for (int j = 0; j < PPT; ++j) {
+        const uint32_t* rp = root + (((by[j] >> s0) << T0) | (bx[j] >> s0));
+        rv[j] = ldg_pred(rp, sv[j] == 0xffffu, sv[j]);
+        c1[j] = (bx[j] & m0) | ((by[j] & m0) << 16);
+      }
+    }
+  }
+  __syncwarp();
+  if (qn) rare_flush(qn);
+  if (blockIdx.x == 0 && tid < (int)(a.n - nmain)) {  // up to 3 trailing points
+    const int64_t i = nmain + tid;
+    const uint64_t qq = quantize_exact(a.xy, i, XY, ox, oy, a.side, a.lim, a.first_bad, a.idx_base);
+    if (qq != ~0ull) {
+      const uint32_t v = index_lookup(a.V, (uint32_t)qq, (uint32_t)(qq >> 32));
+      if (v != 0u) add_owners_g<ATTR>(bins, pool, v, ATTR ? a.attr[i] : 0.f, 0, false, gcnt, gsum);
+    }
+  }
+  asm volatile("bar.sync 1, %0;" ::"r"(NW * 32) : "memory");
+  // flush the hot slots into the global outputs (alpha bin of the slot's region)
+  for (int q = tid; q < NH; q += NW * 32) {
+    uint32_t cnt = 0;
+    long long f = 0;
+    for (int c = 0; c < C; ++c) {
+      const uint32_t* b = h3 + c * P + (ATTR ? 3 * q : q);
+      cnt += b[0];
+      if (ATTR) f += ((long long)(int32_t)b[2] << 16) + (long long)b[1];
+    }
+    if (!cnt) continue;
+    const int32_t r = a.hot_region[q];
+    atomicAdd(&gcnt[2 * r], (unsigned long long)cnt);
+    if (ATTR) atomicAdd(&gsum[2 * r], ldexp((double)(__ldcg(&prow[q]) + f), -Sx));  // drains are L2 REDs
+  }
+}
+
 // binary scale of the SUM fixed point from a strided sample of the attribute
 __global__ void k_attr_scale(const float* attr, int64_t n, int* scale_exp) {
   __shared__ float red[1024];
@@ -1517,6 +1934,39 @@ static cudaError_t warp_dispatch(int ci, const PassArgs& a, size_t smem, cudaStr
   }
 }
 
+template <int XY, bool ATTR, int NW, int PPT, int NST>
+static cudaError_t deep_run(const PassArgs& a, size_t smem, cudaStream_t s, int* blocks, bool launch) {
+  auto kern = k_point_pass_deep<XY, ATTR, NW, PPT, NST>;
+  static int cached_blocks = -1;
+  static size_t cached_smem = 0;
+  if (cached_blocks < 0 || cached_smem != smem) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, RB_SMEM_BUDGET);
+    if (e) return e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NW * 32 + 32, smem);
+    if (e) return e;
+    cached_blocks = per_sm * g_num_sms;
+    cached_smem = smem;
+  }
+  *blocks = cached_blocks;
+  if (!launch || cached_blocks <= 0) return cudaSuccess;
+  kern<<<cached_blocks, NW * 32 + 32, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+// C4 (200M points, 4095 hot slots): 3 stages + 1 hot-slot copy 1.64 ms; 2 stages 1.67; 4 stages 1.73;
+// 2 copies 2.07 (less L1 for the root table); 2048 hot slots 2.35, 1024 2.98 (profiles/round1/deep_sweep.txt)
+static const WarpCfg kDeepCfgs[] = {{16, 4, 3}, {16, 4, 2}, {16, 4, 4}};
+
+template <int XY, bool ATTR>
+static cudaError_t deep_dispatch(int ci, const PassArgs& a, size_t smem, cudaStream_t s, int* blocks, bool launch) {
+  switch (ci) {
+    case 0: return deep_run<XY, ATTR, 16, 4, 3>(a, smem, s, blocks, launch);
+    case 1: return deep_run<XY, ATTR, 16, 4, 2>(a, smem, s, blocks, launch);
+    default: return deep_run<XY, ATTR, 16, 4, 4>(a, smem, s, blocks, launch);
+  }
+}
+
 #define RB_DISPATCH_TMA(FN, GHV, ...)                                                          \
   (dtype == RB_XY_F64 ? (attr ? FN<0, true, GHV>(__VA_ARGS__) : FN<0, false, GHV>(__VA_ARGS__)) \
                       : (attr ? FN<1, true, GHV>(__VA_ARGS__) : FN<1, false, GHV>(__VA_ARGS__)))
@@ -1673,6 +2123,61 @@ int point_pass(const rb_approx* A, const void* xy, int32_t dtype, int64_t n, con
                                                                 attr != nullptr, true, scale, cnt_out, sum_out);
     RB_CUDA(cudaGetLastError());
     ++g_launches;
+    RB_CUDA(cudaFreeAsync(scratch, s));
+    return RB_OK;
+  }
+  // deep-index ring: region sets beyond shared memory, node levels spread over the pipeline
+  int dci = -1;
+  bool nodes32 = true;
+  for (const auto& nb : A->node_bufs) nodes32 = nodes32 && (int64_t)(nb.bytes / 4) < (int64_t(1) << 32);
+  if (use_tma && !smem_hist && L <= 20 && a.V.nlev >= 1 && L - a.V.T0 <= 16 && nodes32 && g_kernel_sel != 3 &&
+      g_kernel_sel != 4) {
+    static int env_dci = -2, env_dc = -2;
+    if (env_dci == -2) {
+      const char* e = getenv("RB_DEEP_CFG");
+      env_dci = e ? atoi(e) : -1;
+      e = getenv("RB_DEEP_COPIES");
+      env_dc = e ? atoi(e) : -1;
+    }
+    const size_t summ_w = A->S >= 0 ? ((size_t)2 << (2 * A->S)) : 16;
+    const int ncfg = (int)(sizeof(kDeepCfgs) / sizeof(kDeepCfgs[0]));
+    const int wpb = attr ? 3 : 1;
+    const int NH = A->n_hot;
+    const int P = NH * wpb + 3 + (int)((33 - (NH * wpb + 3) % 32) % 32);  // P % 32 == 1, >= 3 pad words
+    for (int c = 0; c < ncfg && dci < 0; ++c) {
+      if (env_dci >= 0 && c != env_dci) continue;
+      const WarpCfg& W = kDeepCfgs[c];
+      for (int C = env_dc > 0 ? env_dc : 1; C >= 1; C >>= 1) {  // one copy: the L1 is worth more (root table)
+        const size_t need = (size_t)W.nw * W.nst * W.ppt * 32 * pt_bytes + (size_t)W.nw * 512 + 32 * (attr ? 12 : 4) +
+                            ((((size_t)C * P * 4) + 15) & ~(size_t)15) + summ_w;
+        if (need <= RB_SMEM_BUDGET - 1024) { dci = c; smem = need; a.hcopies = C; a.hstride = P; break; }
+      }
+    }
+    if (dci >= 0) {
+      e = dtype == RB_XY_F64 ? (attr ? deep_dispatch<0, true>(dci, a, smem, s, &blocks, false)
+                                     : deep_dispatch<0, false>(dci, a, smem, s, &blocks, false))
+                             : (attr ? deep_dispatch<1, true>(dci, a, smem, s, &blocks, false)
+                                     : deep_dispatch<1, false>(dci, a, smem, s, &blocks, false));
+      if (e) return cuda_fail(e, "k_point_pass_deep setup");
+      if (blocks <= 0) dci = -1;
+    }
+  }
+  if (dci >= 0) {
+    {
+      const char* e = getenv("RB_FOLD");
+      a.fold = e ? atoi(e) : 0;
+    }
+    void* scratch = nullptr;
+    const size_t rows = (size_t)blocks * std::max(A->n_hot, 1);
+    RB_CUDA(cudaMallocAsync(&scratch, rows * 8 + 16, s));
+    a.part_acc = (long long*)scratch;
+    if (tstart()) return RB_CUDA_ERROR;
+    e = dtype == RB_XY_F64 ? (attr ? deep_dispatch<0, true>(dci, a, smem, s, &blocks, true)
+                                   : deep_dispatch<0, false>(dci, a, smem, s, &blocks, true))
+                           : (attr ? deep_dispatch<1, true>(dci, a, smem, s, &blocks, true)
+                                   : deep_dispatch<1, false>(dci, a, smem, s, &blocks, true));
+    if (e) return cuda_fail(e, "k_point_pass_deep");
+    if (tstop()) return RB_CUDA_ERROR;
     RB_CUDA(cudaFreeAsync(scratch, s));
     return RB_OK;
   }

@@ -10,6 +10,7 @@ run concurrently.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -73,9 +74,11 @@ class ApproxIndex:
                                             N.stream_ptr()), "set_hot")
         self._hot = r.numpy().copy()
 
-    def auto_hot(self, xy, k: int = N.MAX_HOT, sample: int = 1 << 20) -> np.ndarray:
+    def auto_hot(self, xy, k: int | None = None, sample: int = 1 << 20) -> np.ndarray:
         """Pick the k most frequent single owners of a strided point sample."""
         torch = self._torch
+        if k is None:
+            k = int(os.environ.get("RB_HOT_K", N.MAX_HOT))  # RB_HOT_K: experiments
         t, _ = self._xy(xy)
         n = int(t.shape[0])
         if n == 0:

@@ -262,3 +262,38 @@ def test_single_hot_region_copies(oracle_lib):
     idx = _prepared(regions, grid, 0, "trie")
     cnt = _assert_join(idx, A, xy, attr)
     assert cnt[0, 0] == len(xy)
+
+
+@pytest.mark.parametrize("root_level", [8, 6])
+@pytest.mark.parametrize("hot", ["all", "some"])
+def test_deep_index_kernel(oracle_lib, monkeypatch, root_level, hot):
+    """k_point_pass_deep: 3000 regions (histogram beyond shared memory) with two
+    node levels below the root (root level 8 -> node split 1+4, 6 -> 3+4),
+    hot slots for all or only some regions (cold regions and boundary leaves
+    take global REDs), forced drains, out-of-window attributes, clustered
+    points, a trailing partial tile: COUNT bit-exact, SUM within 1e-6."""
+    _gpu()
+    from paper_2010_12548_b200 import workloads as W
+
+    monkeypatch.setenv("RB_FOLD", "2")
+    regions = W.voronoi_tiling(3000, 1.0, seed=4, verts=(10, 30))
+    grid = UNIT.with_level(13)
+    rng = np.random.default_rng(11)
+    n = 1_500_003
+    cen = rng.random((12, 2))
+    xy = np.clip(cen[rng.integers(0, 12, n)] + rng.normal(0, 0.05, (n, 2)), 0.0, 0.999999)
+    attr = rng.lognormal(2.5, 0.6, n).astype(np.float32)
+    k = rng.choice(n, 6000, replace=False)
+    attr[k[:2000]] *= 1e-6
+    attr[k[2000:4000]] = 0.0
+    attr[k[4000:]] *= -1.0
+    for mode in (0, 1):
+        A, _ = oracle_approx(oracle_lib, regions, grid, mode)
+        idx = _prepared(regions, grid, mode, "trie", root_level=root_level)
+        st = idx.stats()
+        assert st["root_level"] == root_level
+        if hot == "some":
+            idx.set_hot(np.arange(0, 3000, 7))
+        _assert_join(idx, A, xy, attr)
+        _assert_join(idx, A, xy.astype(np.float32), attr)
+        _assert_join(idx, A, xy, None)
