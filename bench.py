@@ -218,16 +218,22 @@ def run_ours(a):
     # ncu dram__bytes_read.sum + dram__bytes_write.sum of the point-pass kernel (one --set full
     # capture, profiles/), scaled to this launch's point count; bytes per launch
     traffic = None
+    lookups = None
     prof = os.path.join(ROOT, "profiles", f"ncu_{a.config}_{layout}.json")
     if os.path.exists(prof):
         with open(prof) as f:
             pj = json.load(f)
         if pj.get("dram_bytes_per_point"):
             traffic = round(pj["dram_bytes_per_point"] * n)
+        if pj.get("index_l2_hit_rate") is not None:  # cell-index lookups (evict_normal reads) in that capture
+            lookups = {"l2_hit_rate": round(pj["index_l2_hit_rate"], 4),
+                       "l1_hit_rate": round(pj["index_l1_hit_rate"], 4) if pj.get("index_l1_hit_rate") else None,
+                       "l2_sectors_per_point": round(pj["index_l2_sectors_per_point"], 3),
+                       "source": os.path.relpath(prof, ROOT)}
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
             "kernel": "k_point_pass", "kernel_ms": round(k_ms, 4),
-            "algorithmic_bytes_per_point": C["bpp"], "points_per_launch": n}
+            "algorithmic_bytes_per_point": C["bpp"], "points_per_launch": n, "index_lookups": lookups}
     # ---- e2e: public API on pinned host buffers (rb_join_host), every step
     e2e = None
     if not a.no_e2e:

@@ -33,6 +33,27 @@ rawd = dict(zip(rh, rv))
 for k in ("dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_sector_hit_rate.pct", "gpu__time_duration.sum"):
     if k in rawd:
         summary[k] = (rawd[k], ru[rh.index(k)])
+
+def rawf(k):
+    return float(str(rawd.get(k, "0")).replace(",", "") or 0)
+
+
+# Cell-index lookup hit rates.  The point stream arrives by TMA with an L2 evict_first policy; the only
+# evict_normal reads from the SMs are the index lookups (root / node / owner-pool loads), so the
+# evict_normal read sectors at L2 are the index traffic.  In L1 the global loads are the index loads.
+ih = rawf("lts__t_sectors_srcunit_tex_op_read_evict_normal_lookup_hit.sum")
+im = rawf("lts__t_sectors_srcunit_tex_op_read_evict_normal_lookup_miss.sum")
+lh = rawf("l1tex__t_sectors_pipe_lsu_mem_global_op_ld_lookup_hit.sum")
+lm = rawf("l1tex__t_sectors_pipe_lsu_mem_global_op_ld_lookup_miss.sum")
+index = {}
+if ih + im > 0:
+    index = {"index_l2_hit_rate": ih / (ih + im), "index_l1_hit_rate": lh / (lh + lm) if lh + lm else None,
+             "index_l2_sectors_per_point": (ih + im) / npts if npts else None}
+    summary["index lookups: L2 hit rate"] = (f"{100 * ih / (ih + im):.2f}", "%")
+    if lh + lm:
+        summary["index lookups: L1 hit rate"] = (f"{100 * lh / (lh + lm):.2f}", "%")
+    if npts:
+        summary["index lookups: L2 sectors per point"] = (f"{(ih + im) / npts:.3f}", "")
 for k, (v, u) in summary.items():
     print(f"{k:40s} {v} {u}")
 src = list(csv.reader(io.StringIO(ncu("--page", "source", "--csv", "--print-source", "sass"))))
@@ -74,5 +95,5 @@ if out_json:
     with open(out_json, "w") as f:
         json.dump({"report": rep, "metrics": {k: v for k, (v, u) in summary.items()},
                    "dram_bytes_per_launch": dr, "points": npts,
-                   "dram_bytes_per_point": dr / npts if npts else None,
+                   "dram_bytes_per_point": dr / npts if npts else None, **index,
                    "stalls": {k: v / T for k, v in tot.items()}}, f, indent=1)
