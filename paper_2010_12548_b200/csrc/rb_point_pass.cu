@@ -1893,8 +1893,9 @@ static cudaError_t run_smem(const PassArgs& a, int blocks, size_t smem, cudaStre
 // per-warp-ring kernel configurations (consumer warps, points per lane, stages)
 struct WarpCfg { int nw, ppt, nst; };
 // Preference order.  Shared memory and the L1 data cache share 256 KB per SM, and the carveout is the
-// smallest step (..., 164, 196, 228 KB) that holds the CTA's shared memory: the root / node lookups hit
-// in the L1 that is left.  A 3-stage ring with <= 4 histogram copies (~190 KB for C2 SUM -> 60 KB of
+// smallest step (..., 164, 196, 228 KB) that holds the CTA's shared memory.  The index lookups rarely
+// hit in L1 (1.8 %), but each global load in flight holds an L1 line, so the L1 that is left bounds
+// the lookups in flight.  A 3-stage ring with <= 4 histogram copies (~190 KB for C2 SUM -> 60 KB of
 // L1) beat the 4-stage ring (~220 KB -> 28 KB of L1): 0.475 -> 0.444 ms; forcing the 3-stage ring to a
 // 228 KB carveout gave 0.469 ms.  2 points per lane (0.54 ms), 3 points per lane (0.48 ms) and 2-stage
 // rings (0.47 ms) were slower (profiles/round1/ring_config_sweep.txt).
@@ -1955,7 +1956,7 @@ static cudaError_t deep_run(const PassArgs& a, size_t smem, cudaStream_t s, int*
 }
 
 // C4 (200M points, 4095 hot slots): 3 stages + 1 hot-slot copy 1.64 ms; 2 stages 1.67; 4 stages 1.73;
-// 2 copies 2.07 (less L1 for the root table); 2048 hot slots 2.35, 1024 2.98 (profiles/round1/deep_sweep.txt)
+// 2 copies 2.07 (less L1 for lookups in flight); 2048 hot slots 2.35, 1024 2.98 (profiles/round1/deep_sweep.txt)
 static const WarpCfg kDeepCfgs[] = {{16, 4, 3}, {16, 4, 2}, {16, 4, 4}};
 
 template <int XY, bool ATTR>
