@@ -5,7 +5,8 @@ time, cell count, and the fraction of points whose approximate owner set
 differs from the exact test (the eps-validator checks every such point lies
 within eps of the boundary).  One JSON line per (eps, raster).
 
-usage: python tools/sweep_c3.py [points] [out.jsonl] [validate_sample]"""
+usage: python tools/sweep_c3.py [points] [out.jsonl]
+(the validator is rb_validate_full: every one of the points, not a sample)"""
 import json
 import os
 import sys
@@ -20,11 +21,10 @@ from paper_2010_12548_b200 import workloads as W
 from paper_2010_12548_b200.engine import ApproxIndex
 from paper_2010_12548_b200.geometry import pack_regions
 from paper_2010_12548_b200.grid import level_for_bound
-from paper_2010_12548_b200.validate import validate
+from paper_2010_12548_b200.validate import validate_full
 
 n = int(float(sys.argv[1])) if len(sys.argv) > 1 else 100_000_000
 out = sys.argv[2] if len(sys.argv) > 2 else None
-vs = int(float(sys.argv[3])) if len(sys.argv) > 3 else 200_000
 w = W.c2(n=n)
 packed = pack_regions(w.regions)
 xy = torch.from_numpy(w.xy).cuda()
@@ -62,7 +62,7 @@ for eps in (50.0, 10.0, 4.9, 1.0, 0.5):
         cnt = r.cnt.cpu().numpy()
         if ref_cnt is None:
             ref_cnt = cnt
-        rep = validate(idx, w.xy, eps, max_points=vs)
+        rep = validate_full(idx, xy, eps)
         cells = (st["n_uniform_interior"] + st["n_partial_leaves"]) if raster == "uniform" else \
             (st["n_interior_cells"] + st["n_boundary_cells"])
         rec.update(points_per_s=n / (best / 1e3), pass_ms=round(best, 4), build_ms=round(build_ms, 1),
@@ -71,7 +71,7 @@ for eps in (50.0, 10.0, 4.9, 1.0, 0.5):
                    counts_equal_uniform=bool(np.array_equal(cnt, ref_cnt)),
                    validated_points=rep.points, mismatch_fraction=rep.mismatch_fraction,
                    false_negatives=rep.false_negatives, max_mismatch_distance_m=rep.max_mismatch_distance,
-                   eps_ok=rep.ok)
+                   violations=rep.violations, eps_ok=rep.ok)
         lines.append(rec)
         print(json.dumps(rec), flush=True)
         del idx
