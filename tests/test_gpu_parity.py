@@ -264,11 +264,12 @@ def test_single_hot_region_copies(oracle_lib):
     assert cnt[0, 0] == len(xy)
 
 
-@pytest.mark.parametrize("root_level", [8, 6])
+@pytest.mark.parametrize("root_level,radix_width", [(8, 8), (6, 8), (2, 8), (5, 4)])
 @pytest.mark.parametrize("hot", ["all", "some"])
-def test_deep_index_kernel(oracle_lib, monkeypatch, root_level, hot):
+def test_deep_index_kernel(oracle_lib, monkeypatch, root_level, radix_width, hot):
     """k_point_pass_deep: 3000 regions (histogram beyond shared memory) with two
-    node levels below the root (root level 8 -> node split 1+4, 6 -> 3+4),
+    or more node levels below the root (root level 8 -> node split 1+4, 6 -> 3+4,
+    2 -> 3+4+4, 5 with radix width 4 -> 2+2+2+2),
     hot slots for all or only some regions (cold regions and boundary leaves
     take global REDs), forced drains, out-of-window attributes, clustered
     points, a trailing partial tile: COUNT bit-exact, SUM within 1e-6."""
@@ -289,7 +290,7 @@ def test_deep_index_kernel(oracle_lib, monkeypatch, root_level, hot):
     attr[k[4000:]] *= -1.0
     for mode in (0, 1):
         A, _ = oracle_approx(oracle_lib, regions, grid, mode)
-        idx = _prepared(regions, grid, mode, "trie", root_level=root_level)
+        idx = _prepared(regions, grid, mode, "trie", root_level=root_level, radix_width=radix_width)
         st = idx.stats()
         assert st["root_level"] == root_level
         if hot == "some":
