@@ -222,7 +222,8 @@ int rb_bounds_lookup(const rb_lps* lps, const rb_rs* rs, const uint64_t* lo, con
  * ids non-decreasing; level, Z code at that level, kind 1 = interior /
  * 2 = boundary) -> per region alpha/beta COUNT (device int64 [n_regions*2]) and
  * SUM of prefix attribute attr_idx (device float64 [n_regions*2]; attr_idx < 0:
- * sums left 0).  Cells of one region must be disjoint.  Deterministic. */
+ * sums left 0).  Cells of one region must be disjoint.  Deterministic;
+ * stream-ordered (no host synchronisation). */
 int rb_join_pointindex(const rb_lps* lps, const rb_rs* rs, int64_t n_cells, const int32_t* region,
                        const int32_t* level, const uint64_t* code, const uint8_t* kind, int32_t n_regions,
                        int32_t attr_idx, int64_t* cnt_out, double* sum_out, void* stream);

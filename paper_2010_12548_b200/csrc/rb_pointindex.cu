@@ -217,39 +217,51 @@ __global__ void k_bounds(const uint64_t* codes, int64_t n, RsView rs, int use_rs
   }
 }
 
-// join_pointindex: one warp per region over its (region-sorted) cells, fixed
-// lane-strided order + shuffle tree: deterministic COUNT and SUM
-__global__ void k_join_cells(const uint64_t* codes, int64_t n, RsView rs, int use_rs, const int64_t* cell_beg,
-                             const int32_t* reg, const int32_t* lev, const uint64_t* code, const uint8_t* kind,
-                             int32_t n_regions, int L, const double* prefix, int64_t* cnt_out, double* sum_out) {
-  const int lane = threadIdx.x & 31;
-  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < n_regions;
-       r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    int64_t ca = 0, cb = 0;
-    double sa = 0.0, sb = 0.0;
-    for (int64_t c = cell_beg[r] + lane; c < cell_beg[r + 1]; c += 32) {
-      const int sh = 2 * (L - lev[c]);
-      const uint64_t lo = code[c] << sh, hi = (code[c] + 1) << sh;  // SPEC.md:152-160 cell_interval
-      const int64_t p0 = bound(codes, n, use_rs ? &rs : nullptr, lo);
-      const int64_t p1 = bound(codes, n, use_rs ? &rs : nullptr, hi);
-      const int64_t k = p1 - p0;  // COUNT prefix is the position itself
-      const double s = prefix ? prefix[p1] - prefix[p0] : 0.0;
-      ca += k;
-      sa += s;
-      if (kind[c] == RB_KIND_B) { cb += k; sb += s; }
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-      ca += __shfl_xor_sync(0xffffffffu, ca, o);
-      cb += __shfl_xor_sync(0xffffffffu, cb, o);
-      sa += __shfl_xor_sync(0xffffffffu, sa, o);
-      sb += __shfl_xor_sync(0xffffffffu, sb, o);
-    }
-    if (lane == 0) {
-      cnt_out[2 * r] = ca;
-      cnt_out[2 * r + 1] = cb;
-      sum_out[2 * r] = sa;
-      sum_out[2 * r + 1] = sb;
-    }
+// join_pointindex, pass 1: one thread per covering cell -- its two lower
+// bounds (RadixSpline window or binary search) and the prefix differences
+__global__ void k_cell_vals(const uint64_t* codes, int64_t n, RsView rs, int use_rs, int64_t n_cells,
+                            const int32_t* lev, const uint64_t* code, int L, const double* prefix, int64_t* kv,
+                            double* sv) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n_cells; c += (int64_t)gridDim.x * blockDim.x) {
+    const int sh = 2 * (L - lev[c]);
+    const uint64_t lo = code[c] << sh, hi = (code[c] + 1) << sh;  // SPEC.md:152-160 cell_interval
+    const int64_t p0 = bound(codes, n, use_rs ? &rs : nullptr, lo);
+    const int64_t p1 = bound(codes, n, use_rs ? &rs : nullptr, hi);
+    kv[c] = p1 - p0;  // COUNT prefix is the position itself
+    sv[c] = prefix ? prefix[p1] - prefix[p0] : 0.0;
+  }
+}
+
+// pass 2: one block per region over its (region-grouped) cells, thread-strided
+// order + fixed-order block reduction: deterministic COUNT and SUM
+__global__ void __launch_bounds__(256) k_region_sums(const int64_t* cell_beg, const uint8_t* kind, const int64_t* kv,
+                                                     const double* sv, int64_t* cnt_out, double* sum_out) {
+  __shared__ int64_t sc[2][8];
+  __shared__ double ss[2][8];
+  const int r = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int64_t ca = 0, cb = 0;
+  double sa = 0.0, sb = 0.0;
+  for (int64_t c = cell_beg[r] + threadIdx.x; c < cell_beg[r + 1]; c += 256) {
+    const int64_t k = kv[c];
+    const double v = sv[c];
+    ca += k;
+    sa += v;
+    if (kind[c] == RB_KIND_B) { cb += k; sb += v; }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    ca += __shfl_xor_sync(0xffffffffu, ca, o);
+    cb += __shfl_xor_sync(0xffffffffu, cb, o);
+    sa += __shfl_xor_sync(0xffffffffu, sa, o);
+    sb += __shfl_xor_sync(0xffffffffu, sb, o);
+  }
+  if (lane == 0) { sc[0][warp] = ca; sc[1][warp] = cb; ss[0][warp] = sa; ss[1][warp] = sb; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; ++w) { ca += sc[0][w]; cb += sc[1][w]; sa += ss[0][w]; sb += ss[1][w]; }
+    cnt_out[2 * r] = ca;
+    cnt_out[2 * r + 1] = cb;
+    sum_out[2 * r] = sa;
+    sum_out[2 * r + 1] = sb;
   }
 }
 
@@ -489,6 +501,18 @@ extern "C" int rb_bounds_lookup(const rb_lps* L, const rb_rs* R, const uint64_t*
   return RB_OK;
 }
 
+// stream-ordered scratch (cudaMallocAsync / cudaFreeAsync): no device-wide sync on the query path
+struct SBuf {
+  void* p = nullptr;
+  cudaStream_t s = nullptr;
+  explicit SBuf(cudaStream_t st) : s(st) {}
+  SBuf(const SBuf&) = delete;
+  SBuf& operator=(const SBuf&) = delete;
+  ~SBuf() { if (p) cudaFreeAsync(p, s); }
+  cudaError_t alloc(size_t b) { return cudaMallocAsync(&p, b ? b : 1, s); }
+  template <class T> T* as() const { return (T*)p; }
+};
+
 extern "C" int rb_join_pointindex(const rb_lps* L, const rb_rs* R, int64_t n_cells, const int32_t* region,
                                   const int32_t* level, const uint64_t* code, const uint8_t* kind, int32_t n_regions,
                                   int32_t attr_idx, int64_t* cnt_out, double* sum_out, void* stream) {
@@ -498,7 +522,7 @@ extern "C" int rb_join_pointindex(const rb_lps* L, const rb_rs* R, int64_t n_cel
   if (!cnt_out || !sum_out) return fail(RB_CONFIG_ERROR, "null outputs");
   cudaStream_t s = (cudaStream_t)stream;
   // cells must be grouped by region (non-decreasing region ids): counts -> offsets
-  DBuf beg, off;
+  SBuf beg(s), off(s);
   RB_CUDA(beg.alloc(((int64_t)n_regions + 1) * 8));
   RB_CUDA(off.alloc(((int64_t)n_regions + 1) * 8));
   RB_CUDA(cudaMemsetAsync(beg.p, 0, ((int64_t)n_regions + 1) * 8, s));
@@ -506,18 +530,21 @@ extern "C" int rb_join_pointindex(const rb_lps* L, const rb_rs* R, int64_t n_cel
   size_t tb = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tb, beg.as<int64_t>(), off.as<int64_t>(), n_regions + 1, s);
   {
-    DBuf t;
+    SBuf t(s);
     RB_CUDA(t.alloc(std::max<size_t>(tb, 1)));
     RB_CUDA(cub::DeviceScan::ExclusiveSum(t.p, tb, beg.as<int64_t>(), off.as<int64_t>(), n_regions + 1, s));
-    if (n_regions)
-      k_join_cells<<<nb((int64_t)n_regions * 32), 256, 0, s>>>(
-          L->codes.as<uint64_t>(), L->n, view_of(R), R != nullptr, off.as<int64_t>(), region, level, code, kind,
-          n_regions, L->grid.max_level, attr_idx >= 0 ? L->prefix.as<double>() + (size_t)attr_idx * (L->n + 1) : nullptr,
-          cnt_out, sum_out);
+    SBuf vals(s);
+    RB_CUDA(vals.alloc(std::max<int64_t>(n_cells, 1) * 16));
+    int64_t* kv = vals.as<int64_t>();
+    double* sv = (double*)((char*)vals.p + std::max<int64_t>(n_cells, 1) * 8);
+    if (n_cells)
+      k_cell_vals<<<nb(n_cells), 256, 0, s>>>(
+          L->codes.as<uint64_t>(), L->n, view_of(R), R != nullptr, n_cells, level, code, L->grid.max_level,
+          attr_idx >= 0 ? L->prefix.as<double>() + (size_t)attr_idx * (L->n + 1) : nullptr, kv, sv);
+    if (n_regions) k_region_sums<<<n_regions, 256, 0, s>>>(off.as<int64_t>(), kind, kv, sv, cnt_out, sum_out);
     RB_CUDA(cudaGetLastError());
-    RB_CUDA(cudaStreamSynchronize(s));
   }
-  return RB_OK;
+  return RB_OK;  // stream-ordered: the caller's read of the outputs synchronises
 }
 
 extern "C" int rb_lps_from_arrays(const rb_grid* grid, int64_t n, const uint64_t* codes, const int64_t* perm,
