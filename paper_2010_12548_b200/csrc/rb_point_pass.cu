@@ -887,14 +887,14 @@ __global__ void __launch_bounds__(RB_CONS + 32, RB_MINB_TMA) k_point_pass_tma(Pa
 }
 
 // ---------------------------------------------------------------------------
-// Per-warp TMA rings (the production path for L <= 20 and a shared-memory
+// The TMA ring kernel (the production path for L <= 20 and a shared-memory
 // histogram).
 //
-// Every consumer warp is its own producer: lane 0 streams the warp's next
-// warp-tiles (PPT * 32 points of coordinates + attribute) into the warp's
-// private NST-stage ring with cp.async.bulk and a per-stage mbarrier.  A warp
-// refills a stage as soon as its own lanes have read it, so there is no
-// CTA-wide empty barrier and no producer warp; warps drift independently.
+// One CTA per SM: a producer warp whose lane 0 streams CTA tiles (NW * PPT *
+// 32 points of coordinates + attribute) with cp.async.bulk into an NST-stage
+// shared-memory ring (full / empty mbarriers), and NW consumer warps that run
+// a software pipeline over the tiles (below).  A stage is refilled once all
+// consumer warps have released it.
 //
 // Quantisation, bit-identical to floor(RN((v - o) / side)):
 // t = RN(RN(RN(v - o) * RN(1/side)) + 2^20).  For 0 <= q < 2^20 the high word
@@ -906,10 +906,10 @@ __global__ void __launch_bounds__(RB_CONS + 32, RB_MINB_TMA) k_point_pass_tma(Pa
 //
 // Lookup: level-S summary in shared memory (single owner of a whole summary
 // cell), else the L2-resident root table, then node levels (ACT descent,
-// SPEC.md:285-288).  Accumulation: one interior owner with
-// an in-window attribute -> three predicated u32 shared REDs (count, fixed-
-// point low 16 bits, signed high part); every other owner value on the
-// outlined path.
+// SPEC.md:285-288).  Accumulation: a single owner with an
+// in-window attribute -> three unconditional u32 shared REDs (count, fixed-
+// point low 16 bits, signed high part) into its (region << 1) | boundary bin;
+// owner lists and out-of-window attributes through the per-warp rare queue.
 // ---------------------------------------------------------------------------
 // shared-memory REDs on 32-bit shared addresses (the generic atomicAdd on a
 // pointer the compiler cannot prove shared becomes a generic ATOM)
