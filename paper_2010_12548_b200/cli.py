@@ -229,14 +229,15 @@ def join(points, regions, epsilon, mode, engine, agg, x_col, y_col, out):
         click.echo(text, nl=False)
 
 
-def run_bench(pts, regs, cfg, epsilons, engines, agg, mode, seed, audit_sample=100_000):
+def run_bench(pts, regs, cfg, epsilons, engines, agg, mode, seed, audit_sample=0):
     """per (engine, eps) build + run + audit vs the exact PIP
-    oracle; yields BenchRecord dicts.  Capacity errors are reported per run."""
+    oracle; yields BenchRecord dicts.  Capacity errors are reported per run.
+    audit_sample 0 (default): every point (rb_validate_full); > 0: a seeded sample."""
     from .engine import ApproxIndex
     from .geometry import pack_regions
     from .grid import level_for_bound
     from .query import AggregationQuery
-    from .validate import validate
+    from .validate import validate, validate_full
 
     packed = pack_regions(regs)
     for eps in epsilons:
@@ -247,7 +248,8 @@ def run_bench(pts, regs, cfg, epsilons, engines, agg, mode, seed, audit_sample=1
             t = time.perf_counter()
             idx = ApproxIndex(packed, grid, int(q.mode))
             build_s = time.perf_counter() - t
-            rep = validate(idx, pts.xy, eps, max_points=audit_sample, seed=seed)
+            rep = validate_full(idx, pts.xy, eps) if audit_sample <= 0 else \
+                validate(idx, pts.xy, eps, max_points=audit_sample, seed=seed)
             mem = int(idx.stats()["index_bytes"])
         except E.RasterBoundError as ex:
             yield {"engine": "all", "epsilon": eps, "error": f"{type(ex).__name__}: {ex}"}
@@ -265,7 +267,8 @@ def run_bench(pts, regs, cfg, epsilons, engines, agg, mode, seed, audit_sample=1
                                  "range": r.range} for r in res],
                        audit={"points": rep.points, "mismatch_fraction": rep.mismatch_fraction,
                               "false_negatives": rep.false_negatives,
-                              "max_mismatch_distance": rep.max_mismatch_distance, "eps_ok": rep.ok})
+                              "max_mismatch_distance": rep.max_mismatch_distance, "eps_ok": rep.ok,
+                              "violations": getattr(rep, "violations", None)})
             yield rec
 
 
@@ -300,17 +303,18 @@ def bench(points, regions, epsilons, mode, engine, agg, seed, parallel, out):
 @click.option("--regions", required=True, type=click.Path(exists=True))
 @click.option("--epsilon", required=True, type=float)
 @click.option("--mode", default="conservative")
-@click.option("--sample", default=200_000, type=int)
+@click.option("--sample", default=0, type=int, help="0 (default): every point; N > 0: a seeded sample of N")
 def audit(points, regions, epsilon, mode, sample):
     """Validator: every point assigned differently from the exact test lies within eps."""
     from .engine import ApproxIndex
     from .geometry import pack_regions
     from .grid import level_for_bound
-    from .validate import validate
+    from .validate import validate, validate_full
 
     pts, regs, cfg, _, _ = _load(points, regions)
     grid = cfg.with_level(level_for_bound(cfg, epsilon))
-    rep = validate(ApproxIndex(pack_regions(regs), grid, int(_mode(mode))), pts.xy, epsilon, max_points=sample)
+    idx = ApproxIndex(pack_regions(regs), grid, int(_mode(mode)))
+    rep = validate_full(idx, pts.xy, epsilon) if sample <= 0 else validate(idx, pts.xy, epsilon, max_points=sample)
     click.echo(json.dumps(rep.as_dict()))
 
 
