@@ -247,17 +247,31 @@ def reduce(a: Canvas):
     return int(c[0]), int(c[1]), {k: (float(s[i, 0]), float(s[i, 1])) for i, k in enumerate(a.sum_attrs)}
 
 
+def _compact1by1(v: np.ndarray) -> np.ndarray:
+    """Even bits of Morton codes (x of z_encode)."""
+    v = np.asarray(v, np.uint64) & np.uint64(0x5555555555555555)
+    for sh, m in ((1, 0x3333333333333333), (2, 0x0F0F0F0F0F0F0F0F), (4, 0x00FF00FF00FF00FF),
+                  (8, 0x0000FFFF0000FFFF), (16, 0x00000000FFFFFFFF)):
+        v = (v | (v >> np.uint64(sh))) & np.uint64(m)
+    return v
+
+
 def brj(points, regions, q, cfg: GridConfig, tile_level: int = CANVAS_MAX_LEVEL):
     """The Bounded Raster Join plan written in the canvas algebra:
-    render_points once per tile; per region render_polygon, mask the point
-    canvas by it, reduce (boundary pixels separately into beta).  Tiles of at
-    most 2^13 x 2^13 pixels cover finer grids.  Returns [R,2]
-    alpha/beta COUNT and SUM arrays (dense region order of pack_regions)."""
+    per region, over Z-aligned canvas tiles covering its pixel bounding box
+    (at most 2^tile_level per side): render_points, render_polygon
+    (the region's covering cells), mask the point canvas by it, reduce
+    (boundary pixels separately into beta).  Tiles are sized to the region, so
+    the work is proportional to the region's pixels; the per-tile reductions
+    stay on the device and are summed per region on the host in a fixed order.
+    Returns [R,2] alpha/beta COUNT and SUM arrays (dense region order)."""
     from .engine import ApproxIndex
     from .grid import level_for_bound
     from .pointindex import lps_build
     from .query import _region_cells
 
+    torch = N.require_cuda()
+    lib = N.load()
     ps = as_point_set(points)
     packed = regions if isinstance(regions, PackedRegions) else pack_regions(regions)
     L = level_for_bound(cfg, q.epsilon)
@@ -267,28 +281,60 @@ def brj(points, regions, q, cfg: GridConfig, tile_level: int = CANVAS_MAX_LEVEL)
     lps = lps_build(ps, grid, attrs)
     idx = ApproxIndex(packed, grid, int(q.mode), layout="trie", keep_cells=True)
     region, level, code, kind = _region_cells(packed, idx, L)
+    del idx
     R = packed.n_regions
     beg = np.searchsorted(region, np.arange(R + 1))
-    tl = min(L, tile_level, CANVAS_MAX_LEVEL)
-    nt = 1 << (L - tl)
     cnt = np.zeros((R, 2), np.int64)
     sm = np.zeros((R, 2), np.float64)
-    for ty in range(nt):
-        for tx in range(nt):
-            x0, y0 = tx << tl, ty << tl
-            pc = render_points(None, grid, L, attrs, level=tl, x0=x0, y0=y0, lps=lps)
-            rc = Canvas(grid, L, tl, x0, y0)
-            for r in range(R):
-                if beg[r] == beg[r + 1]:
-                    continue
-                _render_cells(rc, level[beg[r]:beg[r + 1]], code[beg[r]:beg[r + 1]], kind[beg[r]:beg[r + 1]], r)
-                c_all, c_b, sums = reduce(mask(pc, MaskPredicate.covered_by(rc)))
-                cnt[r, 0] += c_all
-                cnt[r, 1] += c_b
-                if attrs:
-                    s_all, s_b = sums[attrs[0]]
-                    sm[r, 0] += s_all
-                    sm[r, 1] += s_b
+    if len(region) == 0:
+        return cnt, sm
+    lv_d = torch.as_tensor(np.asarray(level, np.int32)).cuda()
+    cd_d = torch.as_tensor(np.asarray(code, np.uint64).view(np.int64)).cuda()
+    kd_d = torch.as_tensor(np.asarray(kind, np.uint8)).cuda()
+    # leaf-pixel extent of every cell
+    c64 = np.asarray(code, np.uint64)
+    sh = (L - np.asarray(level, np.int64)).astype(np.int64)
+    cx = _compact1by1(c64).astype(np.int64)
+    cy = _compact1by1(c64 >> np.uint64(1)).astype(np.int64)
+    px0, px1, py0, py1 = cx << sh, (cx + 1) << sh, cy << sh, (cy + 1) << sh
+    cap = min(L, tile_level, CANVAS_MAX_LEVEL)
+    jobs = []
+    for r in range(R):
+        lo, hi = int(beg[r]), int(beg[r + 1])
+        if lo == hi:
+            continue
+        bx0, bx1 = int(px0[lo:hi].min()), int(px1[lo:hi].max())
+        by0, by1 = int(py0[lo:hi].min()), int(py1[lo:hi].max())
+        w = max(bx1 - bx0, by1 - by0)
+        tl = min(cap, max(0, int(math.ceil(math.log2(w)))))
+        for ty in range(by0 >> tl, ((by1 - 1) >> tl) + 1):
+            for tx in range(bx0 >> tl, ((bx1 - 1) >> tl) + 1):
+                jobs.append((r, lo, hi, tl, tx, ty))
+    nsum = max(len(attrs), 1)
+    cnt_t = torch.zeros((len(jobs), 2), dtype=torch.int64, device="cuda")
+    sum_t = torch.zeros((len(jobs), nsum, 2), dtype=torch.float64, device="cuda")
+    canv = {}
+    st = N.stream_ptr()
+    covered = MaskPredicate._CODES["COVERED_BY"]
+    for k, (r, lo, hi, tl, tx, ty) in enumerate(jobs):
+        if tl not in canv:
+            canv[tl] = tuple(Canvas(grid, L, tl, 0, 0, attrs) for _ in range(3))
+        pc, rc, mc = canv[tl]
+        for c in (pc, rc, mc):
+            c.x0, c.y0 = tx << tl, ty << tl
+        dp, dr, dm = pc.desc(), rc.desc(), mc.desc()
+        N.check(lib.rb_canvas_render_points(lps._h, C.byref(dp), st), "render_points")
+        N.check(lib.rb_canvas_render_cells(hi - lo, lv_d[lo:hi].data_ptr(), cd_d[lo:hi].data_ptr(),
+                                           kd_d[lo:hi].data_ptr(), L, int(r), 1, C.byref(dr), st), "render_polygon")
+        N.check(lib.rb_canvas_mask(C.byref(dp), covered, 0, C.byref(dr), C.byref(dm), st), "mask")
+        N.check(lib.rb_canvas_reduce(C.byref(dm), cnt_t[k].data_ptr(), sum_t[k].data_ptr(), st), "reduce")
+    c_h = cnt_t.cpu().numpy()
+    s_h = sum_t.cpu().numpy()
+    for k, job in enumerate(jobs):
+        r = job[0]
+        cnt[r] += c_h[k]
+        if attrs:
+            sm[r] += s_h[k, 0]
     return cnt, sm
 
 

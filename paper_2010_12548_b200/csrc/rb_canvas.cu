@@ -70,6 +70,52 @@ __global__ void k_render_points(const uint64_t* codes, int64_t n, const double* 
     }
   }
 }
+// Z-aligned tiles: the leaves of an aligned 2^lev x 2^lev block are the Z-code
+// range [zlo, zlo + 4^lev), so only that slice of the sorted codes is visited.
+__device__ __forceinline__ uint64_t spread1by1(uint64_t v) {
+  v &= 0xffffffffull;
+  v = (v | (v << 16)) & 0x0000ffff0000ffffull;
+  v = (v | (v << 8)) & 0x00ff00ff00ff00ffull;
+  v = (v | (v << 4)) & 0x0f0f0f0f0f0f0f0full;
+  v = (v | (v << 2)) & 0x3333333333333333ull;
+  v = (v | (v << 1)) & 0x5555555555555555ull;
+  return v;
+}
+__global__ void k_tile_range(const uint64_t* codes, int64_t n, int64_t x0, int64_t y0, int lev, int64_t* range) {
+  const uint64_t zlo = spread1by1((uint64_t)x0) | (spread1by1((uint64_t)y0) << 1);
+  const uint64_t zhi = zlo + ((uint64_t)1 << (2 * lev));
+  for (int b = 0; b < 2; ++b) {
+    const uint64_t key = b ? zhi : zlo;
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+      const int64_t m = (lo + hi) >> 1;
+      if (codes[m] < key) lo = m + 1; else hi = m;
+    }
+    range[b] = lo;
+  }
+}
+__global__ void k_render_points_range(const uint64_t* codes, int64_t n, const int64_t* range, const double* prefix,
+                                      int n_attr, int L, int64_t x0, int64_t y0, int lev, int64_t* count,
+                                      double* sums) {
+  const int64_t W = (int64_t)1 << lev;
+  const int64_t b = range[0], e = range[1];
+  for (int64_t i = b + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < e; i += (int64_t)gridDim.x * blockDim.x) {
+    if (i > b && codes[i] == codes[i - 1]) continue;
+    const uint64_t c = codes[i];
+    const int64_t ix = (int64_t)compact1by1(c) - x0, iy = (int64_t)compact1by1(c >> 1) - y0;
+    int64_t lo = i + 1, hi = e;  // run end within the tile's slice
+    while (lo < hi) {
+      const int64_t m = (lo + hi) >> 1;
+      if (codes[m] <= c) lo = m + 1; else hi = m;
+    }
+    const int64_t p = iy * W + ix;
+    count[p] = lo - i;
+    for (int s = 0; s < n_attr; ++s) {
+      const double* pre = prefix + (size_t)s * (n + 1);
+      sums[(size_t)s * W * W + p] = pre[lo] - pre[i];
+    }
+  }
+}
 __global__ void k_flag_nonempty(int64_t n, const int64_t* count, uint8_t* flags) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     flags[i] = count[i] > 0 ? RB_PX_VALID : 0u;
@@ -253,8 +299,20 @@ extern "C" int rb_canvas_render_points(const rb_lps* lps, rb_canvas_desc* out, v
   if (out->level > L) return fail(RB_SHAPE_ERROR, "canvas tile finer than the point index level");
   cudaStream_t s = (cudaStream_t)stream;
   k_canvas_clear<<<cb(npx(out)), 256, 0, s>>>(npx(out), out->n_sum, out->count, out->sums, out->region, out->flags);
-  if (n) k_render_points<<<cb(n), 256, 0, s>>>(codes, n, prefix, out->n_sum, L, out->x0, out->y0, out->level,
-                                              out->count, out->sums);
+  const int64_t W = (int64_t)1 << out->level;
+  const bool aligned = out->x0 >= 0 && out->y0 >= 0 && (out->x0 % W) == 0 && (out->y0 % W) == 0 &&
+                       out->x0 + W <= ((int64_t)1 << L) && out->y0 + W <= ((int64_t)1 << L);
+  if (n && aligned) {  // only the tile's slice of the sorted codes
+    int64_t* range = nullptr;
+    RB_CUDA(cudaMallocAsync(&range, 16, s));
+    k_tile_range<<<1, 1, 0, s>>>(codes, n, out->x0, out->y0, out->level, range);
+    k_render_points_range<<<cb(std::min<int64_t>(n, (int64_t)npx(out) * 4)), 256, 0, s>>>(
+        codes, n, range, prefix, out->n_sum, L, out->x0, out->y0, out->level, out->count, out->sums);
+    RB_CUDA(cudaFreeAsync(range, s));
+  } else if (n) {
+    k_render_points<<<cb(n), 256, 0, s>>>(codes, n, prefix, out->n_sum, L, out->x0, out->y0, out->level, out->count,
+                                          out->sums);
+  }
   k_flag_nonempty<<<cb(npx(out)), 256, 0, s>>>(npx(out), out->count, out->flags);
   RB_CUDA(cudaGetLastError());
   return RB_OK;
@@ -320,13 +378,14 @@ extern "C" int rb_canvas_affine(const rb_canvas_desc* a, int64_t dx, int64_t dy,
 extern "C" int rb_canvas_reduce(const rb_canvas_desc* a, int64_t* cnt_out, double* sum_out, void* stream) {
   if (!desc_ok(a) || !cnt_out || (a->n_sum && !sum_out)) return fail(RB_CONFIG_ERROR, "invalid argument");
   cudaStream_t s = (cudaStream_t)stream;
-  DBuf pc, ps;
-  RB_CUDA(pc.alloc(RB_RED_BLOCKS * 16));
-  RB_CUDA(ps.alloc((size_t)std::max(a->n_sum, 1) * RB_RED_BLOCKS * 16));
-  k_reduce_px<<<RB_RED_BLOCKS, 256, 0, s>>>(npx(a), a->n_sum, a->count, a->sums, a->flags, pc.as<long long>(),
-                                            ps.as<double>());
-  k_reduce_px2<<<1, 32, 0, s>>>(RB_RED_BLOCKS, a->n_sum, pc.as<long long>(), ps.as<double>(), cnt_out, sum_out);
+  long long* pc = nullptr;
+  double* ps = nullptr;  // stream-ordered scratch: no host synchronisation
+  RB_CUDA(cudaMallocAsync(&pc, RB_RED_BLOCKS * 16, s));
+  RB_CUDA(cudaMallocAsync(&ps, (size_t)std::max(a->n_sum, 1) * RB_RED_BLOCKS * 16, s));
+  k_reduce_px<<<RB_RED_BLOCKS, 256, 0, s>>>(npx(a), a->n_sum, a->count, a->sums, a->flags, pc, ps);
+  k_reduce_px2<<<1, 32, 0, s>>>(RB_RED_BLOCKS, a->n_sum, pc, ps, cnt_out, sum_out);
   RB_CUDA(cudaGetLastError());
-  RB_CUDA(cudaStreamSynchronize(s));  // pc/ps are released on return
+  RB_CUDA(cudaFreeAsync(pc, s));
+  RB_CUDA(cudaFreeAsync(ps, s));
   return RB_OK;
 }

@@ -263,8 +263,10 @@ def _region_cells(packed: PackedRegions, index: ApproxIndex, L: int):
             keep[j] = True
             cur_r, cur_hi, cur_j = r, hi[j], j
         region, level, code, kind = region[keep], level[keep], code[keep], kind[keep]
-    o = np.argsort(region, kind="stable")
-    return region[o], level[o].astype(np.int32), code[o], kind[o].astype(np.uint8)
+    if len(region) > 1 and not np.all(region[1:] >= region[:-1]):  # cells come grouped by polygon already
+        o = np.argsort(region, kind="stable")
+        region, level, code, kind = region[o], level[o], code[o], kind[o]
+    return region, level.astype(np.int32), code, kind.astype(np.uint8)
 
 
 class PreparedPointIndexJoin:
