@@ -2,7 +2,7 @@
 """bench.py -- points/s of the epsilon-bounded point-polygon COUNT/SUM join
 (BASELINE.json metric) on B200, plus the reference CPU path.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c4|c1] [--layout trie|dense]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c4|c1] [--layout trie|dense|keys]
   python bench.py --impl reference ...        (CPU oracle port on the host cores)
 
 One step = one point pass over this rank's batch of synthetic points (inputs
@@ -48,7 +48,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
-    ap.add_argument("--layout", default=None, choices=["trie", "dense"])
+    ap.add_argument("--layout", default=None, choices=["trie", "dense", "keys"])
     ap.add_argument("--points", type=int, default=None, help="override points per GPU")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

@@ -45,6 +45,8 @@ extern "C" {
 /* cell-index layouts (north star subsystem 2) */
 #define RB_LAYOUT_DENSE 0 /* dense leaf grid of owner values (uniform raster)   */
 #define RB_LAYOUT_TRIE 1  /* multi-level radix table (ACT, hierarchical raster) */
+#define RB_LAYOUT_KEYS 2  /* sorted 64-bit cell keys (disjoint covering cells, leaf-level start keys)
+                           with a radix table over the top key bits: radix + binary search */
 
 /* point coordinate storage */
 #define RB_XY_F64 0 /* interleaved float64 (x,y) */

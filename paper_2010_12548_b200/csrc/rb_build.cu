@@ -517,6 +517,17 @@ __global__ void k_split(Recs in, int64_t n, const int64_t* split, const int64_t*
   }
 }
 // owners per position: distinct regions (records sorted by region, kind within position; I=1 first)
+// RB_LAYOUT_KEYS radix table: tab[p] = first key index with key >> shift >= p
+__global__ void k_key_table(const uint64_t* keys, int64_t n, int shift, int64_t nslots, uint32_t* tab) {
+  GRID_STRIDE(p, nslots) {
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+      const int64_t m = (lo + hi) >> 1;
+      if ((keys[m] >> shift) < (uint64_t)p) lo = m + 1; else hi = m;
+    }
+    tab[p] = (uint32_t)lo;
+  }
+}
 __global__ void k_pos_owners(Recs r, int64_t n, const int64_t* pbeg, int64_t npos, int64_t* nown) {
   GRID_STRIDE(P, npos) {
     int64_t b = pbeg[P], e = (P + 1 < npos) ? pbeg[P + 1] : n;
@@ -792,6 +803,35 @@ static int index_impl(int L, int64_t total_cells, const int32_t* cp_in, const ui
     A->stats.n_positions = npos;
   }
   rs.release(); rl.release(); rr.release(); rk.release(); head.release(); hpos.release(); pb.release();
+
+  if (opts->layout == RB_LAYOUT_KEYS) {
+    // sorted 64-bit cell keys: the disjoint positions already come sorted by start key
+    A->T0 = 0;
+    A->k = std::max(1, opts->radix_width / 2);
+    A->nkeys = npos;
+    int bits = 1;
+    while (bits < 2 * L && ((int64_t)1 << bits) < 2 * std::max<int64_t>(npos, 1)) ++bits;
+    bits = std::min(bits, std::min(2 * L, 24));
+    bits = std::max(bits, 1);
+    A->kshift = 2 * L - bits;
+    const int64_t nslots = ((int64_t)1 << bits) + 1;
+    RB_CUDA(A->ktab.alloc(nslots * 4));
+    k_key_table<<<nblk(nslots), 256, 0, s>>>(pstart.as<uint64_t>(), npos, A->kshift, nslots, A->ktab.as<uint32_t>());
+    RB_CUDA(cudaGetLastError());
+    A->keys = std::move(pstart);
+    A->klev = std::move(plevel);
+    A->kval = std::move(pval);
+    RB_CUDA(A->root.alloc(4));  // unused (no radix table levels)
+    RB_CUDA(cudaMemsetAsync(A->root.p, 0, 4, s));
+    A->root_entries = 1;
+    A->S = -1;
+    A->stats.root_level = 0;
+    A->stats.node_levels = 0;
+    A->stats.n_nodes = 0;
+    A->stats.index_bytes = npos * 13 + nslots * 4 + npool * 4;
+    RB_CUDA(cudaStreamSynchronize(s));
+    return RB_OK;
+  }
 
   // ---- index geometry
   int k = std::max(1, opts->radix_width / 2);
@@ -1203,7 +1243,8 @@ extern "C" int rb_approx_build(const rb_grid* grid, const rb_polygons* polys, co
     return fail(RB_CONFIG_ERROR, "grid extent must be finite and > 0");
   if (opts->mode != RB_MODE_CONSERVATIVE && opts->mode != RB_MODE_CENTER_SAMPLED)
     return fail(RB_CONFIG_ERROR, "unknown raster mode");
-  if (opts->layout != RB_LAYOUT_DENSE && opts->layout != RB_LAYOUT_TRIE) return fail(RB_CONFIG_ERROR, "unknown layout");
+  if (opts->layout != RB_LAYOUT_DENSE && opts->layout != RB_LAYOUT_TRIE && opts->layout != RB_LAYOUT_KEYS)
+    return fail(RB_CONFIG_ERROR, "unknown layout");
   if (opts->radix_width != 2 && opts->radix_width != 4 && opts->radix_width != 8)
     return fail(RB_CONFIG_ERROR, "radix_width must be 2, 4 or 8 (SPEC.md:278)");
   if (polys->n_regions <= 0 || polys->n_regions >= (1 << 29)) return fail(RB_CAPACITY_ERROR, "n_regions outside [1, 2^29)");
@@ -1240,7 +1281,8 @@ extern "C" int rb_index_from_cells(const rb_grid* grid, int64_t n_cells, const i
   if (!grid || !opts || !out) return fail(RB_CONFIG_ERROR, "null argument");
   *out = nullptr;
   if (grid->max_level < 0 || grid->max_level > 31) return fail(RB_CAPACITY_ERROR, "max_level outside [0, 31]");
-  if (opts->layout != RB_LAYOUT_DENSE && opts->layout != RB_LAYOUT_TRIE) return fail(RB_CONFIG_ERROR, "unknown layout");
+  if (opts->layout != RB_LAYOUT_DENSE && opts->layout != RB_LAYOUT_TRIE && opts->layout != RB_LAYOUT_KEYS)
+    return fail(RB_CONFIG_ERROR, "unknown layout");
   if (opts->radix_width != 2 && opts->radix_width != 4 && opts->radix_width != 8)
     return fail(RB_CONFIG_ERROR, "radix_width must be 2, 4 or 8 (SPEC.md:278)");
   if (n_regions <= 0 || n_regions >= (1 << 29)) return fail(RB_CAPACITY_ERROR, "n_regions outside [1, 2^29)");

@@ -188,12 +188,49 @@ struct IndexView {
   const uint16_t* summary;  // level-S table of single owner values (0xffff = consult the index)
   int S;
   int64_t nodes0_len;  // entries of the first node level (32-bit offsets when < 2^32)
+  // RB_LAYOUT_KEYS: disjoint cells as sorted leaf-level start keys, their levels and owner values,
+  // and a radix table over the top key bits (ktab[p] = first key with key >> kshift >= p)
+  const uint64_t* keys;
+  const uint8_t* klev;
+  const uint32_t* kval;
+  const uint32_t* ktab;
+  int64_t nkeys;
+  int kshift;
 };
+
+__device__ __forceinline__ uint64_t spread_bits(uint32_t v) {
+  uint64_t x = v;
+  x = (x | (x << 16)) & 0x0000ffff0000ffffull;
+  x = (x | (x << 8)) & 0x00ff00ff00ff00ffull;
+  x = (x | (x << 4)) & 0x0f0f0f0f0f0f0f0full;
+  x = (x | (x << 2)) & 0x3333333333333333ull;
+  x = (x | (x << 1)) & 0x5555555555555555ull;
+  return x;
+}
+
+// RB_LAYOUT_KEYS lookup: the leaf's Z code (x in the even bits), the radix table
+// narrows the sorted keys to one prefix bucket (plus the key before it), a binary search finds the
+// last cell starting at or before the leaf, and the leaf is owned iff it lies inside that cell.
+__device__ __forceinline__ uint32_t keys_lookup(const IndexView& v, uint32_t ix, uint32_t iy) {
+  const uint64_t z = spread_bits(ix) | (spread_bits(iy) << 1);
+  const uint64_t p = z >> v.kshift;
+  int64_t lo = (int64_t)v.ktab[p], hi = (int64_t)v.ktab[p + 1];
+  lo = lo > 0 ? lo - 1 : 0;
+  while (lo < hi) {
+    const int64_t m = (lo + hi) >> 1;
+    if (v.keys[m] <= z) lo = m + 1; else hi = m;
+  }
+  const int64_t c = lo - 1;
+  if (c < 0) return 0u;
+  const uint64_t end = v.keys[c] + ((uint64_t)1 << (2 * (v.L - (int)v.klev[c])));
+  return z < end ? v.kval[c] : 0u;
+}
 
 // Owner value of leaf (ix, iy): descend the radix table (ACT lookup,
 // every terminal on the path is collected; after the overlay
 // a slot holds either a child pointer or the complete owner value).
 __device__ __forceinline__ uint32_t index_lookup(const IndexView& v, uint32_t ix, uint32_t iy) {
+  if (v.keys) return keys_lookup(v, ix, iy);
   int s = v.L - v.T0;
   uint32_t val = __ldg(&v.root[((size_t)(iy >> s) << v.T0) | (ix >> s)]);
 #pragma unroll
@@ -223,6 +260,9 @@ struct rb_approx {
   int T0 = 0, k = 4;
   rb::DBuf summary;  // u16 [4^S] or empty
   int S = -1;
+  rb::DBuf keys, klev, kval, ktab;  // RB_LAYOUT_KEYS
+  int64_t nkeys = 0;
+  int kshift = 0;
   rb::DBuf hot_region;  // int32 [n_hot]: hot slot -> region
   int32_t n_hot = 0;
   // optional exports
@@ -242,6 +282,12 @@ struct rb_approx {
     v.summary = summary.as<uint16_t>();
     v.S = S;
     v.nodes0_len = v.nlev > 0 ? (int64_t)(node_bufs[0].bytes / 4) : 0;
+    v.keys = keys.as<uint64_t>();
+    v.klev = klev.as<uint8_t>();
+    v.kval = kval.as<uint32_t>();
+    v.ktab = ktab.as<uint32_t>();
+    v.nkeys = nkeys;
+    v.kshift = kshift;
     return v;
   }
 };

@@ -493,11 +493,17 @@ __global__ void __launch_bounds__(256, RB_MINB) k_point_pass(PassArgs a) {
           }
         }
       }
-      // 2. root reads for all points, then node levels (ACT descent)
+      // 2. root reads for all points, then node levels (ACT descent); the sorted-key
+      //    layout (RB_LAYOUT_KEYS) instead searches its keys per point
+      if (a.V.keys) {
 #pragma unroll
-      for (int i = 0; i < RB_PB; ++i) {
-        const uint32_t ri = ((iy[i] >> c.s0) << c.T0) | (ix[i] >> c.s0);
-        val[i] = (okm >> i) & 1u ? __ldg(c.root + ri) : 0u;
+        for (int i = 0; i < RB_PB; ++i) val[i] = (okm >> i) & 1u ? keys_lookup(a.V, ix[i], iy[i]) : 0u;
+      } else {
+#pragma unroll
+        for (int i = 0; i < RB_PB; ++i) {
+          const uint32_t ri = ((iy[i] >> c.s0) << c.T0) | (ix[i] >> c.s0);
+          val[i] = (okm >> i) & 1u ? __ldg(c.root + ri) : 0u;
+        }
       }
       uint32_t nodem = 0;
 #pragma unroll
@@ -2023,7 +2029,7 @@ int point_pass(const rb_approx* A, const void* xy, int32_t dtype, int64_t n, con
   const size_t hot_bins = (((size_t)A->n_hot * (attr ? 12 : 4)) + 15) & ~(size_t)15;
   const bool aligned = ((uintptr_t)xy % 16 == 0) && (!attr || (uintptr_t)attr % 16 == 0);
   const bool vec = ((uintptr_t)xy % 32 == 0) && (!attr || (uintptr_t)attr % (dtype == RB_XY_F64 ? 8 : 16) == 0);
-  const bool use_tma = g_kernel_sel != 0 && aligned;
+  const bool use_tma = g_kernel_sel != 0 && aligned && !A->keys.p;  // sorted-key layout: k_point_pass / _global
   // histogram placement: every bin in shared memory when it fits next to the ring
   const bool smem_hist = use_tma ? ring + all_bins + summ_bytes <= RB_SMEM_BUDGET
                                  : (size_t)R2 * (attr ? 28 : 4) <= RB_SMEM_BUDGET;

@@ -21,7 +21,7 @@ from .geometry import DevicePolygons, PackedRegions
 from .grid import GridConfig
 
 INT64_MAX = (1 << 63) - 1
-LAYOUTS = {"dense": N.LAYOUT_DENSE, "trie": N.LAYOUT_TRIE}
+LAYOUTS = {"dense": N.LAYOUT_DENSE, "trie": N.LAYOUT_TRIE, "keys": N.LAYOUT_KEYS}
 
 
 @dataclass
@@ -44,7 +44,7 @@ class ApproxIndex:
                  stream=None):
         torch = N.require_cuda()
         if layout not in LAYOUTS:
-            raise E.ConfigError(f"unknown layout {layout!r} (dense | trie)")
+            raise E.ConfigError(f"unknown layout {layout!r} (dense | trie | keys)")
         self.packed = packed
         self.grid = grid
         self.mode = int(mode)
@@ -146,7 +146,7 @@ class ApproxIndex:
         torch = self._torch
         t, dt = self._xy(xy)
         n = int(t.shape[0])
-        if self._hot is None and self.n_regions > self.HOT_THRESHOLD:
+        if self._hot is None and self.n_regions > self.HOT_THRESHOLD and self.layout != "keys":
             self.auto_hot(t)
         a = None
         if attr is not None:
@@ -166,7 +166,7 @@ class ApproxIndex:
     def join_host(self, xy: np.ndarray, attr: np.ndarray | None = None):
         """rb_join_host: host (ideally pinned) buffers in, host results out."""
         xy = np.ascontiguousarray(xy) if isinstance(xy, np.ndarray) else xy
-        if self._hot is None and self.n_regions > self.HOT_THRESHOLD:
+        if self._hot is None and self.n_regions > self.HOT_THRESHOLD and self.layout != "keys":
             step = max(1, int(xy.shape[0]) // (1 << 20))
             self.auto_hot(xy[::step])
         if isinstance(xy, np.ndarray):

@@ -298,3 +298,32 @@ def test_deep_index_kernel(oracle_lib, monkeypatch, root_level, radix_width, hot
         _assert_join(idx, A, xy, attr)
         _assert_join(idx, A, xy.astype(np.float32), attr)
         _assert_join(idx, A, xy, None)
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_sorted_key_layout(oracle_lib, mode):
+    """RB_LAYOUT_KEYS (sorted 64-bit cell keys + radix table over the top key
+    bits): overlapping polygons with holes (owner lists), the C2 generator
+    (SUM), and 3000 regions (global histogram), f64 and f32 points; plus
+    act_lookup and the complete validator through the same index."""
+    torch = _gpu()
+    from paper_2010_12548_b200 import workloads as W
+    from paper_2010_12548_b200.grid import level_for_bound
+    from paper_2010_12548_b200.validate import validate_full
+
+    rng = np.random.default_rng(21)
+    cases = [(random_polygons(8, 25, holes=True), UNIT.with_level(11), rng.random((400_003, 2)), None)]
+    w = W.c2(n=1_000_001)
+    cases.append((w.regions, w.grid.with_level(level_for_bound(w.grid, w.epsilon)), w.xy, w.attrs["fare"]))
+    cases.append((W.voronoi_tiling(3000, 1.0, seed=4, verts=(10, 30)), UNIT.with_level(12), rng.random((300_001, 2)),
+                  rng.lognormal(2.5, 0.6, 300_001).astype(np.float32)))
+    for regions, grid, xy, attr in cases:
+        A, _ = oracle_approx(oracle_lib, regions, grid, mode)
+        idx = _prepared(regions, grid, mode, "keys")
+        _assert_join(idx, A, xy, attr)
+        _assert_join(idx, A, xy.astype(np.float32), None)
+        trie = _prepared(regions, grid, mode, "trie")
+        sample = xy[:50_000]
+        assert torch.equal(idx.lookup(sample), trie.lookup(sample))
+    rep = validate_full(idx, xy, 1.0 / (1 << 12))
+    assert rep.owner_set_overflows == 0
