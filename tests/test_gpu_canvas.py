@@ -133,3 +133,33 @@ def test_brj_algebra_equals_join_act(oracle_lib, seed):
                 np.testing.assert_allclose(sm, [[r.alpha, r.boundary_part] for r in ref], rtol=1e-6, atol=1e-6)
             alg = join_canvas(pts, regions, q, cfg=UNIT, plan="algebra")
             assert [r.alpha for r in alg] == pytest.approx([r.alpha for r in ref], rel=1e-6)
+
+
+def test_render_points_tiles_aligned_and_unaligned():
+    """Sub-tiles of the point canvas: Z-aligned tiles (only the tile's slice of
+    the sorted codes is visited) and unaligned or edge-clipped offsets (full
+    scan) both equal the matching window of the whole-grid canvas."""
+    _gpu()
+    from paper_2010_12548_b200 import canvas as CV
+    from paper_2010_12548_b200.geometry import PointSet
+    from paper_2010_12548_b200.pointindex import lps_build
+
+    L = 9
+    rng = np.random.default_rng(3)
+    xy = rng.random((300_000, 2)) ** 2  # skewed towards the origin
+    w = rng.lognormal(2.5, 0.6, len(xy)).astype(np.float32)
+    ps = PointSet(xy, {"w": w})
+    lps = lps_build(ps, UNIT.with_level(L), ["w"])
+    full = CV.render_points(None, UNIT, L, ["w"], lps=lps)
+    fc, fs = full.count.cpu().numpy(), full.sum("w").cpu().numpy()
+    for lev, x0, y0 in ((6, 0, 0), (6, 64, 128), (5, 480, 480), (4, 3, 5), (6, 500, 7), (3, 0, 511)):
+        t = CV.render_points(None, UNIT, L, ["w"], level=lev, x0=x0, y0=y0, lps=lps)
+        W = 1 << lev
+        wc = np.zeros((W, W), np.int64)
+        ws = np.zeros((W, W))
+        hx, hy = min(W, (1 << L) - x0), min(W, (1 << L) - y0)
+        wc[:hy, :hx] = fc[y0:y0 + hy, x0:x0 + hx]
+        ws[:hy, :hx] = fs[y0:y0 + hy, x0:x0 + hx]
+        np.testing.assert_array_equal(t.count.cpu().numpy(), wc)
+        np.testing.assert_allclose(t.sum("w").cpu().numpy(), ws, rtol=1e-12, atol=1e-9)
+        assert bool(((t.count > 0) == ~t.empty).all())
