@@ -952,7 +952,7 @@ __device__ __forceinline__ void add_owners_w(uint32_t bins, double* slow, const 
   }
 }
 
-template <int XY, bool ATTR, int NW, int PPT, int NST>
+template <int XY, bool ATTR, int NW, int PPT, int NST, bool KEYS = false>
 __global__ void __launch_bounds__(NW * 32 + 32, NW <= 8 ? 2 : 1) k_point_pass_ring(PassArgs a) {
   constexpr int PB = XY == 0 ? 16 : 8;
   constexpr int WT = PPT * 32;  // points per consumer warp per tile
@@ -1261,6 +1261,10 @@ __global__ void __launch_bounds__(NW * 32 + 32, NW <= 8 ? 2 : 1) k_point_pass_ri
           }
         }
       }
+      if constexpr (KEYS) {  // RB_LAYOUT_KEYS: radix bucket + binary search of the sorted cell keys
+#pragma unroll
+        for (int j = 0; j < PPT; ++j) rv[j] = (killm >> j) & 1u ? 0u : keys_lookup(a.V, bx[j], by[j]);
+      } else {
       // summary (shared memory), else the radix table (L2)
       uint32_t sv[PPT];
 #pragma unroll
@@ -1274,6 +1278,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, NW <= 8 ? 2 : 1) k_point_pass_ri
       for (int j = 0; j < PPT; ++j) {
         const uint32_t* rp = root + (((by[j] >> s0) << T0) | (bx[j] >> s0));
         rv[j] = ldg_pred(rp, sv[j] == 0xffffu, sv[j]);
+      }
       }
     }
   }
@@ -1907,9 +1912,9 @@ struct WarpCfg { int nw, ppt, nst; };
 // rings (0.47 ms) were slower (profiles/round1/ring_config_sweep.txt).
 static const WarpCfg kWarpCfgs[] = {{16, 4, 3}, {16, 4, 4}, {16, 4, 2}, {15, 4, 2}};
 
-template <int XY, bool ATTR, int NW, int PPT, int NST>
+template <int XY, bool ATTR, int NW, int PPT, int NST, bool KEYS = false>
 static cudaError_t warp_run(const PassArgs& a, size_t smem, cudaStream_t s, int* blocks, bool launch) {
-  auto kern = k_point_pass_ring<XY, ATTR, NW, PPT, NST>;
+  auto kern = k_point_pass_ring<XY, ATTR, NW, PPT, NST, KEYS>;
   static int cached_blocks = -1;
   static size_t cached_smem = 0;
   if (cached_blocks < 0 || cached_smem != smem) {
@@ -1931,8 +1936,9 @@ static cudaError_t warp_run(const PassArgs& a, size_t smem, cudaStream_t s, int*
   return cudaGetLastError();
 }
 
-template <int XY, bool ATTR>
+template <int XY, bool ATTR, bool KEYS = false>
 static cudaError_t warp_dispatch(int ci, const PassArgs& a, size_t smem, cudaStream_t s, int* blocks, bool launch) {
+  if constexpr (KEYS) return warp_run<XY, ATTR, 16, 4, 3, true>(a, smem, s, blocks, launch);  // the default shape only
   switch (ci) {
     case 0: return warp_run<XY, ATTR, 16, 4, 3>(a, smem, s, blocks, launch);
     case 1: return warp_run<XY, ATTR, 16, 4, 4>(a, smem, s, blocks, launch);
@@ -2029,7 +2035,8 @@ int point_pass(const rb_approx* A, const void* xy, int32_t dtype, int64_t n, con
   const size_t hot_bins = (((size_t)A->n_hot * (attr ? 12 : 4)) + 15) & ~(size_t)15;
   const bool aligned = ((uintptr_t)xy % 16 == 0) && (!attr || (uintptr_t)attr % 16 == 0);
   const bool vec = ((uintptr_t)xy % 32 == 0) && (!attr || (uintptr_t)attr % (dtype == RB_XY_F64 ? 8 : 16) == 0);
-  const bool use_tma = g_kernel_sel != 0 && aligned && !A->keys.p;  // sorted-key layout: k_point_pass / _global
+  const bool keys = A->keys.p != nullptr;  // RB_LAYOUT_KEYS: the ring kernel (KEYS) or the generic kernels
+  const bool use_tma = g_kernel_sel != 0 && aligned && !keys;
   // histogram placement: every bin in shared memory when it fits next to the ring
   const bool smem_hist = use_tma ? ring + all_bins + summ_bytes <= RB_SMEM_BUDGET
                                  : (size_t)R2 * (attr ? 28 : 4) <= RB_SMEM_BUDGET;
@@ -2063,7 +2070,7 @@ int point_pass(const rb_approx* A, const void* xy, int32_t dtype, int64_t n, con
   size_t smem = 0;
   // per-warp rings: shared-memory histogram, L <= 20 (the 2^20 quantisation window)
   int wci = -1;
-  if (use_tma && smem_hist && L <= 20 && g_kernel_sel != 3) {
+  if (g_kernel_sel != 0 && aligned && smem_hist && L <= 20 && g_kernel_sel != 3) {
     static int env_ci = -2;
     if (env_ci == -2) {
       const char* e = getenv("RB_WARP_CFG");
@@ -2081,6 +2088,7 @@ int point_pass(const rb_approx* A, const void* xy, int32_t dtype, int64_t n, con
     // more L1 (carveout) than they save in RED conflicts
     for (int c = 0; c < ncfg && wci < 0; ++c) {
       if (env_ci >= 0 && c != env_ci) continue;
+      if (keys && c != 0) continue;  // the KEYS ring is instantiated for the default shape only
       const WarpCfg& W = kWarpCfgs[c];
       const int wpb = attr ? 3 : 1;
       const int P = R2 * wpb + 3 + (int)((33 - (R2 * wpb + 3) % 32) % 32);  // P % 32 == 1, >= 3 pad words
@@ -2092,10 +2100,14 @@ int point_pass(const rb_approx* A, const void* xy, int32_t dtype, int64_t n, con
       }
     }
     if (wci >= 0) {
-      e = dtype == RB_XY_F64 ? (attr ? warp_dispatch<0, true>(wci, a, smem, s, &blocks, false)
-                                     : warp_dispatch<0, false>(wci, a, smem, s, &blocks, false))
-                             : (attr ? warp_dispatch<1, true>(wci, a, smem, s, &blocks, false)
-                                     : warp_dispatch<1, false>(wci, a, smem, s, &blocks, false));
+      e = keys ? (dtype == RB_XY_F64 ? (attr ? warp_dispatch<0, true, true>(wci, a, smem, s, &blocks, false)
+                                             : warp_dispatch<0, false, true>(wci, a, smem, s, &blocks, false))
+                                     : (attr ? warp_dispatch<1, true, true>(wci, a, smem, s, &blocks, false)
+                                             : warp_dispatch<1, false, true>(wci, a, smem, s, &blocks, false)))
+               : (dtype == RB_XY_F64 ? (attr ? warp_dispatch<0, true>(wci, a, smem, s, &blocks, false)
+                                             : warp_dispatch<0, false>(wci, a, smem, s, &blocks, false))
+                                     : (attr ? warp_dispatch<1, true>(wci, a, smem, s, &blocks, false)
+                                             : warp_dispatch<1, false>(wci, a, smem, s, &blocks, false)));
       if (e) return cuda_fail(e, "k_point_pass_ring setup");
       if (blocks <= 0) wci = -1;
     }
@@ -2120,10 +2132,14 @@ int point_pass(const rb_approx* A, const void* xy, int32_t dtype, int64_t n, con
     int* scale = (int*)((char*)scratch + rows * 20);
     a.scale_exp = scale;  // written by the ring kernel (CTA 0) for k_reduce_fixed
     if (tstart()) return RB_CUDA_ERROR;
-    e = dtype == RB_XY_F64 ? (attr ? warp_dispatch<0, true>(wci, a, smem, s, &blocks, true)
-                                   : warp_dispatch<0, false>(wci, a, smem, s, &blocks, true))
-                           : (attr ? warp_dispatch<1, true>(wci, a, smem, s, &blocks, true)
-                                   : warp_dispatch<1, false>(wci, a, smem, s, &blocks, true));
+    e = keys ? (dtype == RB_XY_F64 ? (attr ? warp_dispatch<0, true, true>(wci, a, smem, s, &blocks, true)
+                                           : warp_dispatch<0, false, true>(wci, a, smem, s, &blocks, true))
+                                   : (attr ? warp_dispatch<1, true, true>(wci, a, smem, s, &blocks, true)
+                                           : warp_dispatch<1, false, true>(wci, a, smem, s, &blocks, true)))
+             : (dtype == RB_XY_F64 ? (attr ? warp_dispatch<0, true>(wci, a, smem, s, &blocks, true)
+                                           : warp_dispatch<0, false>(wci, a, smem, s, &blocks, true))
+                                   : (attr ? warp_dispatch<1, true>(wci, a, smem, s, &blocks, true)
+                                           : warp_dispatch<1, false>(wci, a, smem, s, &blocks, true)));
     if (e) return cuda_fail(e, "k_point_pass_ring");
     if (tstop()) return RB_CUDA_ERROR;
     k_reduce_fixed<<<std::max(1, (R2 + 31) / 32), 1024, 0, s>>>(a.part_cnt, a.part_acc, a.part_sum, blocks, R2,
