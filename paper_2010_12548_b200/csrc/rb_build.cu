@@ -517,6 +517,37 @@ __global__ void k_split(Recs in, int64_t n, const int64_t* split, const int64_t*
   }
 }
 // owners per position: distinct regions (records sorted by region, kind within position; I=1 first)
+// RB_LAYOUT_KEYS records: start key, owner value and level of each disjoint cell in one uint4
+__global__ void k_key_records(const uint64_t* start, const uint8_t* level, const uint32_t* val, int64_t n,
+                              uint4* rec) {
+  GRID_STRIDE(i, n) rec[i] = make_uint4((uint32_t)start[i], (uint32_t)(start[i] >> 32), val[i], level[i]);
+}
+// RB_LAYOUT_KEYS summary: a level-S block is answered by one owner value when a single cell covers
+// it (value <= 0xfffe: single owners), 0 when no cell meets it, else 0xffff (consult the keys)
+__global__ void k_key_summary(const uint4* rec, int64_t n, int L, int S, uint16_t* out) {
+  GRID_STRIDE(b, (int64_t)1 << (2 * S)) {
+    const uint64_t span = (uint64_t)1 << (2 * (L - S));
+    const uint32_t bx = (uint32_t)(b & ((1 << S) - 1)), by = (uint32_t)(b >> S);  // row-major, as the kernels read it
+    const uint64_t z0 = spread_bits(bx << (L - S)) | (spread_bits(by << (L - S)) << 1), z1 = z0 + span;
+    int64_t lo = 0, hi = n;  // first cell with start > z0
+    while (lo < hi) {
+      const int64_t m = (lo + hi) >> 1;
+      if ((((uint64_t)rec[m].y << 32) | rec[m].x) <= z0) lo = m + 1; else hi = m;
+    }
+    uint16_t v = 0xffffu;
+    const int64_t c = lo - 1;
+    const uint64_t nxt = lo < n ? (((uint64_t)rec[lo].y << 32) | rec[lo].x) : ~0ull;
+    if (c >= 0) {
+      const uint64_t st = ((uint64_t)rec[c].y << 32) | rec[c].x;
+      const uint64_t en = st + ((uint64_t)1 << (2 * (L - (int)rec[c].w)));
+      if (en >= z1) v = rec[c].z <= 0xfffeu ? (uint16_t)rec[c].z : 0xffffu;  // one cell covers the block
+      else if (en <= z0 && nxt >= z1) v = 0;                                   // no cell meets the block
+    } else if (nxt >= z1) {
+      v = 0;
+    }
+    out[b] = v;
+  }
+}
 // RB_LAYOUT_KEYS radix table: tab[p] = first key index with key >> shift >= p
 __global__ void k_key_table(const uint64_t* keys, int64_t n, int shift, int64_t nslots, uint32_t* tab) {
   GRID_STRIDE(p, nslots) {
@@ -818,17 +849,29 @@ static int index_impl(int L, int64_t total_cells, const int32_t* cp_in, const ui
     RB_CUDA(A->ktab.alloc(nslots * 4));
     k_key_table<<<nblk(nslots), 256, 0, s>>>(pstart.as<uint64_t>(), npos, A->kshift, nslots, A->ktab.as<uint32_t>());
     RB_CUDA(cudaGetLastError());
-    A->keys = std::move(pstart);
-    A->klev = std::move(plevel);
-    A->kval = std::move(pval);
+    RB_CUDA(A->keys.alloc(std::max<int64_t>(npos, 1) * 16));
+    if (npos) k_key_records<<<nblk(npos), 256, 0, s>>>(pstart.as<uint64_t>(), plevel.as<uint8_t>(), pval.as<uint32_t>(),
+                                                       npos, A->keys.as<uint4>());
     RB_CUDA(A->root.alloc(4));  // unused (no radix table levels)
     RB_CUDA(cudaMemsetAsync(A->root.p, 0, 4, s));
     A->root_entries = 1;
     A->S = -1;
+    {  // level-S summary for the shared-memory fast path, as for the radix table
+      int Smax = RB_SUMMARY_DEFAULT;
+      if (const char* e = getenv("RB_SUMMARY_LEVEL")) Smax = std::min(atoi(e), 8);
+      if (Smax >= 0 && 2 * (int64_t)A->n_regions + 1 < 0xffff) {
+        const int S = std::min(Smax, L);
+        RB_CUDA(A->summary.alloc(((size_t)2 << (2 * S))));
+        k_key_summary<<<nblk((int64_t)1 << (2 * S)), 256, 0, s>>>(A->keys.as<uint4>(), npos, L, S,
+                                                                  A->summary.as<uint16_t>());
+        RB_CUDA(cudaGetLastError());
+        A->S = S;
+      }
+    }
     A->stats.root_level = 0;
     A->stats.node_levels = 0;
     A->stats.n_nodes = 0;
-    A->stats.index_bytes = npos * 13 + nslots * 4 + npool * 4;
+    A->stats.index_bytes = npos * 16 + nslots * 4 + npool * 4;
     RB_CUDA(cudaStreamSynchronize(s));
     return RB_OK;
   }

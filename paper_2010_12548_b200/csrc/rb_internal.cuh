@@ -190,9 +190,7 @@ struct IndexView {
   int64_t nodes0_len;  // entries of the first node level (32-bit offsets when < 2^32)
   // RB_LAYOUT_KEYS: disjoint cells as sorted leaf-level start keys, their levels and owner values,
   // and a radix table over the top key bits (ktab[p] = first key with key >> kshift >= p)
-  const uint64_t* keys;
-  const uint8_t* klev;
-  const uint32_t* kval;
+  const uint4* krec;    // per cell: start key (lo, hi words), owner value, level -- one 16-byte load
   const uint32_t* ktab;
   int64_t nkeys;
   int kshift;
@@ -208,29 +206,47 @@ __device__ __forceinline__ uint64_t spread_bits(uint32_t v) {
   return x;
 }
 
-// RB_LAYOUT_KEYS lookup: the leaf's Z code (x in the even bits), the radix table
-// narrows the sorted keys to one prefix bucket (plus the key before it), a binary search finds the
-// last cell starting at or before the leaf, and the leaf is owned iff it lies inside that cell.
-__device__ __forceinline__ uint32_t keys_lookup(const IndexView& v, uint32_t ix, uint32_t iy) {
-  const uint64_t z = spread_bits(ix) | (spread_bits(iy) << 1);
-  const uint64_t p = z >> v.kshift;
-  int64_t lo = (int64_t)v.ktab[p], hi = (int64_t)v.ktab[p + 1];
+// RB_LAYOUT_KEYS lookup: the leaf's Z code (x in the even bits); the radix table
+// narrows the sorted cells to one prefix bucket (plus the cell before it).  Buckets hold ~1 cell, so
+// the few records are read at once (one dependent step after the table); larger buckets binary-search.
+// The owner is the last cell starting at or before the leaf, if the leaf lies inside it.
+__device__ __forceinline__ uint64_t leaf_z(uint32_t ix, uint32_t iy) { return spread_bits(ix) | (spread_bits(iy) << 1); }
+
+// the owner of leaf z among the cells [lo, hi) of its radix bucket (lo = table[p], hi = table[p + 1])
+__device__ __forceinline__ uint32_t keys_resolve(const IndexView& v, uint64_t z, int64_t lo, int64_t hi) {
   lo = lo > 0 ? lo - 1 : 0;
-  while (lo < hi) {
-    const int64_t m = (lo + hi) >> 1;
-    if (v.keys[m] <= z) lo = m + 1; else hi = m;
+  uint4 best = make_uint4(0u, 0u, 0u, 0u);
+  bool found = false;
+  if (hi - lo <= 4) {
+    uint4 r[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) r[t] = lo + t < hi ? __ldg(v.krec + lo + t) : make_uint4(0xffffffffu, 0xffffffffu, 0u, 0u);
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const uint64_t k = ((uint64_t)r[t].y << 32) | r[t].x;
+      if (lo + t < hi && k <= z) { best = r[t]; found = true; }
+    }
+  } else {
+    while (lo < hi) {
+      const int64_t m = (lo + hi) >> 1;
+      const uint4 rm = __ldg(v.krec + m);
+      if ((((uint64_t)rm.y << 32) | rm.x) <= z) { best = rm; found = true; lo = m + 1; } else hi = m;
+    }
   }
-  const int64_t c = lo - 1;
-  if (c < 0) return 0u;
-  const uint64_t end = v.keys[c] + ((uint64_t)1 << (2 * (v.L - (int)v.klev[c])));
-  return z < end ? v.kval[c] : 0u;
+  if (!found) return 0u;
+  const uint64_t start = ((uint64_t)best.y << 32) | best.x;
+  const uint64_t end = start + ((uint64_t)1 << (2 * (v.L - (int)best.w)));
+  return z < end ? best.z : 0u;
 }
 
-// Owner value of leaf (ix, iy): descend the radix table (ACT lookup,
-// every terminal on the path is collected; after the overlay
-// a slot holds either a child pointer or the complete owner value).
+__device__ __forceinline__ uint32_t keys_lookup(const IndexView& v, uint32_t ix, uint32_t iy) {
+  const uint64_t z = leaf_z(ix, iy);
+  const uint64_t p = z >> v.kshift;
+  return keys_resolve(v, z, (int64_t)v.ktab[p], (int64_t)v.ktab[p + 1]);
+}
+
 __device__ __forceinline__ uint32_t index_lookup(const IndexView& v, uint32_t ix, uint32_t iy) {
-  if (v.keys) return keys_lookup(v, ix, iy);
+  if (v.krec) return keys_lookup(v, ix, iy);
   int s = v.L - v.T0;
   uint32_t val = __ldg(&v.root[((size_t)(iy >> s) << v.T0) | (ix >> s)]);
 #pragma unroll
@@ -260,7 +276,7 @@ struct rb_approx {
   int T0 = 0, k = 4;
   rb::DBuf summary;  // u16 [4^S] or empty
   int S = -1;
-  rb::DBuf keys, klev, kval, ktab;  // RB_LAYOUT_KEYS
+  rb::DBuf keys, ktab;  // RB_LAYOUT_KEYS: uint4 records (start key, owner value, level), radix table
   int64_t nkeys = 0;
   int kshift = 0;
   rb::DBuf hot_region;  // int32 [n_hot]: hot slot -> region
@@ -282,9 +298,7 @@ struct rb_approx {
     v.summary = summary.as<uint16_t>();
     v.S = S;
     v.nodes0_len = v.nlev > 0 ? (int64_t)(node_bufs[0].bytes / 4) : 0;
-    v.keys = keys.as<uint64_t>();
-    v.klev = klev.as<uint8_t>();
-    v.kval = kval.as<uint32_t>();
+    v.krec = keys.as<uint4>();
     v.ktab = ktab.as<uint32_t>();
     v.nkeys = nkeys;
     v.kshift = kshift;

@@ -495,7 +495,7 @@ __global__ void __launch_bounds__(256, RB_MINB) k_point_pass(PassArgs a) {
       }
       // 2. root reads for all points, then node levels (ACT descent); the sorted-key
       //    layout (RB_LAYOUT_KEYS) instead searches its keys per point
-      if (a.V.keys) {
+      if (a.V.krec) {
 #pragma unroll
         for (int i = 0; i < RB_PB; ++i) val[i] = (okm >> i) & 1u ? keys_lookup(a.V, ix[i], iy[i]) : 0u;
       } else {
@@ -1100,6 +1100,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, NW <= 8 ? 2 : 1) k_point_pass_ri
     __syncwarp();
   };
   uint32_t rv[PPT], bx[PPT], by[PPT], nv[PPT];
+  uint32_t hv[PPT];  // KEYS: radix bucket end (rv = bucket start, ~0u = no lookup)
   float w1[PPT], w2[PPT];
 #pragma unroll
   for (int j = 0; j < PPT; ++j) { rv[j] = bx[j] = by[j] = nv[j] = 0u; w1[j] = w2[j] = 0.f; }
@@ -1168,6 +1169,15 @@ __global__ void __launch_bounds__(NW * 32 + 32, NW <= 8 ? 2 : 1) k_point_pass_ri
       }
     }
     // ------------------------------------------------------------ B(k-1)
+    if constexpr (KEYS) {  // the bucket's cell records for the bucket read in A(k-1)
+      if (k >= 1 && k <= K) {
+#pragma unroll
+        for (int j = 0; j < PPT; ++j) {
+          w2[j] = w1[j];
+          nv[j] = hv[j] == ~0u ? rv[j] : keys_resolve(a.V, leaf_z(bx[j], by[j]), (int64_t)rv[j], (int64_t)hv[j]);
+        }
+      }
+    } else
     if (k >= 1 && k <= K) {
 #pragma unroll
       for (int j = 0; j < PPT; ++j) w2[j] = w1[j];
@@ -1261,9 +1271,15 @@ __global__ void __launch_bounds__(NW * 32 + 32, NW <= 8 ? 2 : 1) k_point_pass_ri
           }
         }
       }
-      if constexpr (KEYS) {  // RB_LAYOUT_KEYS: radix bucket + binary search of the sorted cell keys
+      if constexpr (KEYS) {  // RB_LAYOUT_KEYS: summary, else the radix bucket now and its cell records in B(k)
 #pragma unroll
-        for (int j = 0; j < PPT; ++j) rv[j] = (killm >> j) & 1u ? 0u : keys_lookup(a.V, bx[j], by[j]);
+        for (int j = 0; j < PPT; ++j) {
+          uint32_t sv = summ[((by[j] >> sS) << S) | (bx[j] >> sS)];
+          if ((killm >> j) & 1u) sv = 0u;
+          const uint64_t p = leaf_z(bx[j], by[j]) >> a.V.kshift;
+          rv[j] = ldg_pred(a.V.ktab + p, sv == 0xffffu, sv);     // bucket start, or the answered value
+          hv[j] = ldg_pred(a.V.ktab + p + 1, sv == 0xffffu, ~0u);  // bucket end, or ~0u: answered
+        }
       } else {
       // summary (shared memory), else the radix table (L2)
       uint32_t sv[PPT];
