@@ -842,7 +842,7 @@ static int index_impl(int L, int64_t total_cells, const int32_t* cp_in, const ui
     A->nkeys = npos;
     int bits = 1;
     while (bits < 2 * L && ((int64_t)1 << bits) < 2 * std::max<int64_t>(npos, 1)) ++bits;
-    bits = std::min(bits, std::min(2 * L, 24));
+    bits = std::min(bits, std::min(2 * L, 29));  // ~1 cell per bucket up to 2^28 cells (a 2 GB table)
     bits = std::max(bits, 1);
     A->kshift = 2 * L - bits;
     const int64_t nslots = ((int64_t)1 << bits) + 1;
@@ -1379,6 +1379,15 @@ __global__ void k_hot_values(uint32_t* v, int64_t n, const int32_t* remap) {
     v[k] = code | ((uint32_t)remap[r] << RB_HOT_SHIFT);
   }
 }
+// RB_LAYOUT_KEYS: annotate the single owner values of the cell records
+__global__ void k_hot_records(uint4* rec, int64_t n, const int32_t* remap) {
+  GRID_STRIDE(k, n) {
+    const uint32_t x = rec[k].z;
+    if (x == 0u || (x & (RB_VALUE_NODE | RB_VALUE_LIST))) continue;
+    const uint32_t code = x & RB_CODE_MASK;
+    rec[k].z = code | ((uint32_t)remap[(code - 1u) >> 1] << RB_HOT_SHIFT);
+  }
+}
 // annotate owner-list entries ((region<<1)|boundary); count words are flagged
 __global__ void k_hot_pool(uint32_t* p, int64_t n, const int32_t* remap) {
   GRID_STRIDE(k, n) {
@@ -1425,7 +1434,12 @@ extern "C" int rb_approx_set_hot(rb_approx* a, const int32_t* regions, int32_t n
   }
   if (a->pool_len) k_hot_pool<<<nblk(a->pool_len), 256, 0, s>>>(a->pool.as<uint32_t>(), a->pool_len, remap.as<int32_t>());
   RB_CUDA(cudaGetLastError());
-  if (a->S >= 0)  // annotated values exceed u16: the summary refers them to the index
+  if (a->keys.p && a->nkeys)
+    k_hot_records<<<nblk(a->nkeys), 256, 0, s>>>(a->keys.as<uint4>(), a->nkeys, remap.as<int32_t>());
+  if (a->S >= 0 && a->keys.p)  // annotated values exceed u16: the summary refers them to the index
+    k_key_summary<<<nblk((int64_t)1 << (2 * a->S)), 256, 0, s>>>(a->keys.as<uint4>(), a->nkeys, a->grid.max_level,
+                                                                 a->S, a->summary.as<uint16_t>());
+  else if (a->S >= 0)
     k_summary<<<nblk(((int64_t)32 << (2 * a->S))), 256, 0, s>>>(a->root.as<uint32_t>(), a->T0, a->S,
                                                                  a->summary.as<uint16_t>());
   RB_CUDA(cudaGetLastError());

@@ -1396,7 +1396,7 @@ __device__ __forceinline__ void redg_sum(double* p, double w, bool pred) {
                : "memory");
 }
 
-template <int XY, bool ATTR, int NW, int PPT, int NST>
+template <int XY, bool ATTR, int NW, int PPT, int NST, bool KEYS = false>
 __global__ void __launch_bounds__(NW * 32 + 32, 1) k_point_pass_deep(PassArgs a) {
   constexpr int PB = XY == 0 ? 16 : 8;
   constexpr int WT = PPT * 32;
@@ -1526,6 +1526,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) k_point_pass_deep(PassArgs a)
     __syncwarp();
   };
   uint32_t rv[PPT], c1[PPT], c2[PPT], nv1[PPT], nv2[PPT];
+  uint32_t hv[PPT], zh[PPT];  // KEYS: radix bucket end (~0u: answered) and the leaf code's high word (c1: low word)
   float w1[PPT], w2[PPT], w3[PPT];
 #pragma unroll
   for (int j = 0; j < PPT; ++j) { rv[j] = c1[j] = c2[j] = nv1[j] = nv2[j] = 0u; w1[j] = w2[j] = w3[j] = 0.f; }
@@ -1597,6 +1598,12 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) k_point_pass_deep(PassArgs a)
       }
     }
     // ------------------------------------------------------------ B2(k-2): node levels 1..
+    if constexpr (KEYS) {
+      if (k >= 2 && k <= K + 1) {
+#pragma unroll
+        for (int j = 0; j < PPT; ++j) { w3[j] = w2[j]; nv2[j] = nv1[j]; }
+      }
+    } else
     if (k >= 2 && k <= K + 1) {
 #pragma unroll
       for (int j = 0; j < PPT; ++j) { w3[j] = w2[j]; nv2[j] = nv1[j]; }
@@ -1629,6 +1636,16 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) k_point_pass_deep(PassArgs a)
       }
     }
     // ------------------------------------------------------------ B1(k-1): node level 0
+    if constexpr (KEYS) {  // RB_LAYOUT_KEYS: the bucket's cell records
+      if (k >= 1 && k <= K) {
+#pragma unroll
+        for (int j = 0; j < PPT; ++j) {
+          w2[j] = w1[j];
+          nv1[j] = hv[j] == ~0u ? rv[j]
+                                : keys_resolve(a.V, ((uint64_t)zh[j] << 32) | c1[j], (int64_t)rv[j], (int64_t)hv[j]);
+        }
+      }
+    } else
     if (k >= 1 && k <= K) {
 #pragma unroll
       for (int j = 0; j < PPT; ++j) { w2[j] = w1[j]; c2[j] = c1[j]; }
@@ -1710,11 +1727,23 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) k_point_pass_deep(PassArgs a)
         for (int j = 0; j < PPT; ++j)
           if (killm & (1u << j)) sv[j] = 0u;
       }
+      if constexpr (KEYS) {  // the radix bucket now, its records in B1
+#pragma unroll
+        for (int j = 0; j < PPT; ++j) {
+          const uint64_t z = leaf_z(bx[j], by[j]);
+          const uint64_t p = z >> a.V.kshift;
+          rv[j] = ldg_pred(a.V.ktab + p, sv[j] == 0xffffu, sv[j]);
+          hv[j] = ldg_pred(a.V.ktab + p + 1, sv[j] == 0xffffu, ~0u);
+          c1[j] = (uint32_t)z;
+          zh[j] = (uint32_t)(z >> 32);
+        }
+      } else {
 #pragma unroll
       for (int j = 0; j < PPT; ++j) {
         const uint32_t* rp = root + (((by[j] >> s0) << T0) | (bx[j] >> s0));
         rv[j] = ldg_pred(rp, sv[j] == 0xffffu, sv[j]);
         c1[j] = (bx[j] & m0) | ((by[j] & m0) << 16);
+      }
       }
     }
   }
@@ -1963,9 +1992,9 @@ static cudaError_t warp_dispatch(int ci, const PassArgs& a, size_t smem, cudaStr
   }
 }
 
-template <int XY, bool ATTR, int NW, int PPT, int NST>
+template <int XY, bool ATTR, int NW, int PPT, int NST, bool KEYS = false>
 static cudaError_t deep_run(const PassArgs& a, size_t smem, cudaStream_t s, int* blocks, bool launch) {
-  auto kern = k_point_pass_deep<XY, ATTR, NW, PPT, NST>;
+  auto kern = k_point_pass_deep<XY, ATTR, NW, PPT, NST, KEYS>;
   static int cached_blocks = -1;
   static size_t cached_smem = 0;
   if (cached_blocks < 0 || cached_smem != smem) {
@@ -1987,8 +2016,9 @@ static cudaError_t deep_run(const PassArgs& a, size_t smem, cudaStream_t s, int*
 // 2 copies 2.07 (less L1 for lookups in flight); 2048 hot slots 2.35, 1024 2.98 (profiles/round1/deep_sweep.txt)
 static const WarpCfg kDeepCfgs[] = {{16, 4, 3}, {16, 4, 2}, {16, 4, 4}};
 
-template <int XY, bool ATTR>
+template <int XY, bool ATTR, bool KEYS = false>
 static cudaError_t deep_dispatch(int ci, const PassArgs& a, size_t smem, cudaStream_t s, int* blocks, bool launch) {
+  if constexpr (KEYS) return deep_run<XY, ATTR, 16, 4, 3, true>(a, smem, s, blocks, launch);  // default shape only
   switch (ci) {
     case 0: return deep_run<XY, ATTR, 16, 4, 3>(a, smem, s, blocks, launch);
     case 1: return deep_run<XY, ATTR, 16, 4, 2>(a, smem, s, blocks, launch);
@@ -2075,7 +2105,8 @@ int point_pass(const rb_approx* A, const void* xy, int32_t dtype, int64_t n, con
     return RB_OK;
   };
   cudaError_t e = cudaSuccess;
-  if (!smem_hist && !use_tma) {  // fallback for misaligned inputs with large region sets
+  const bool keys_deep = keys && g_kernel_sel != 0 && aligned && L <= 20 && g_kernel_sel != 3 && g_kernel_sel != 4;
+  if (!smem_hist && !use_tma && !keys_deep) {  // fallback for misaligned inputs with large region sets
     const int blocks = g_num_sms * 4;
     if (tstart()) return RB_CUDA_ERROR;
     e = dtype == RB_XY_F64 ? launch_a<0, false>(a, vec, blocks, 0, s) : launch_a<1, false>(a, vec, blocks, 0, s);
@@ -2169,8 +2200,8 @@ int point_pass(const rb_approx* A, const void* xy, int32_t dtype, int64_t n, con
   int dci = -1;
   bool nodes32 = true;
   for (const auto& nb : A->node_bufs) nodes32 = nodes32 && (int64_t)(nb.bytes / 4) < (int64_t(1) << 32);
-  if (use_tma && !smem_hist && L <= 20 && a.V.nlev >= 1 && L - a.V.T0 <= 16 && nodes32 && g_kernel_sel != 3 &&
-      g_kernel_sel != 4) {
+  const bool deep_shape = keys || (a.V.nlev >= 1 && L - a.V.T0 <= 16 && nodes32);
+  if (g_kernel_sel != 0 && aligned && !smem_hist && L <= 20 && deep_shape && g_kernel_sel != 3 && g_kernel_sel != 4) {
     static int env_dci = -2, env_dc = -2;
     if (env_dci == -2) {
       const char* e = getenv("RB_DEEP_CFG");
@@ -2185,6 +2216,7 @@ int point_pass(const rb_approx* A, const void* xy, int32_t dtype, int64_t n, con
     const int P = NH * wpb + 3 + (int)((33 - (NH * wpb + 3) % 32) % 32);  // P % 32 == 1, >= 3 pad words
     for (int c = 0; c < ncfg && dci < 0; ++c) {
       if (env_dci >= 0 && c != env_dci) continue;
+      if (keys && c != 0) continue;  // the KEYS variant exists for the default shape only
       const WarpCfg& W = kDeepCfgs[c];
       for (int C = env_dc > 0 ? env_dc : 1; C >= 1; C >>= 1) {  // one copy: the L1 is worth more (root table)
         const size_t need = (size_t)W.nw * W.nst * W.ppt * 32 * pt_bytes + (size_t)W.nw * 512 + 32 * (attr ? 12 : 4) +
@@ -2193,10 +2225,14 @@ int point_pass(const rb_approx* A, const void* xy, int32_t dtype, int64_t n, con
       }
     }
     if (dci >= 0) {
-      e = dtype == RB_XY_F64 ? (attr ? deep_dispatch<0, true>(dci, a, smem, s, &blocks, false)
-                                     : deep_dispatch<0, false>(dci, a, smem, s, &blocks, false))
-                             : (attr ? deep_dispatch<1, true>(dci, a, smem, s, &blocks, false)
-                                     : deep_dispatch<1, false>(dci, a, smem, s, &blocks, false));
+      e = keys ? (dtype == RB_XY_F64 ? (attr ? deep_dispatch<0, true, true>(dci, a, smem, s, &blocks, false)
+                                             : deep_dispatch<0, false, true>(dci, a, smem, s, &blocks, false))
+                                     : (attr ? deep_dispatch<1, true, true>(dci, a, smem, s, &blocks, false)
+                                             : deep_dispatch<1, false, true>(dci, a, smem, s, &blocks, false)))
+               : (dtype == RB_XY_F64 ? (attr ? deep_dispatch<0, true>(dci, a, smem, s, &blocks, false)
+                                             : deep_dispatch<0, false>(dci, a, smem, s, &blocks, false))
+                                     : (attr ? deep_dispatch<1, true>(dci, a, smem, s, &blocks, false)
+                                             : deep_dispatch<1, false>(dci, a, smem, s, &blocks, false)));
       if (e) return cuda_fail(e, "k_point_pass_deep setup");
       if (blocks <= 0) dci = -1;
     }
@@ -2211,14 +2247,24 @@ int point_pass(const rb_approx* A, const void* xy, int32_t dtype, int64_t n, con
     RB_CUDA(cudaMallocAsync(&scratch, rows * 8 + 16, s));
     a.part_acc = (long long*)scratch;
     if (tstart()) return RB_CUDA_ERROR;
-    e = dtype == RB_XY_F64 ? (attr ? deep_dispatch<0, true>(dci, a, smem, s, &blocks, true)
-                                   : deep_dispatch<0, false>(dci, a, smem, s, &blocks, true))
-                           : (attr ? deep_dispatch<1, true>(dci, a, smem, s, &blocks, true)
-                                   : deep_dispatch<1, false>(dci, a, smem, s, &blocks, true));
+    e = keys ? (dtype == RB_XY_F64 ? (attr ? deep_dispatch<0, true, true>(dci, a, smem, s, &blocks, true)
+                                           : deep_dispatch<0, false, true>(dci, a, smem, s, &blocks, true))
+                                   : (attr ? deep_dispatch<1, true, true>(dci, a, smem, s, &blocks, true)
+                                           : deep_dispatch<1, false, true>(dci, a, smem, s, &blocks, true)))
+             : (dtype == RB_XY_F64 ? (attr ? deep_dispatch<0, true>(dci, a, smem, s, &blocks, true)
+                                           : deep_dispatch<0, false>(dci, a, smem, s, &blocks, true))
+                                   : (attr ? deep_dispatch<1, true>(dci, a, smem, s, &blocks, true)
+                                           : deep_dispatch<1, false>(dci, a, smem, s, &blocks, true)));
     if (e) return cuda_fail(e, "k_point_pass_deep");
     if (tstop()) return RB_CUDA_ERROR;
     RB_CUDA(cudaFreeAsync(scratch, s));
     return RB_OK;
+  }
+  if (!smem_hist && !use_tma) {  // sorted-key layout whose deep kernel did not fit: global histogram
+    if (tstart()) return RB_CUDA_ERROR;
+    e = dtype == RB_XY_F64 ? launch_a<0, false>(a, vec, g_num_sms * 4, 0, s) : launch_a<1, false>(a, vec, g_num_sms * 4, 0, s);
+    if (e) return cuda_fail(e, "k_point_pass_global");
+    return tstop();
   }
   if (use_tma) {
     smem = ring + (smem_hist ? all_bins : hot_bins) + summ_bytes;

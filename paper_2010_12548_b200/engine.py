@@ -146,7 +146,7 @@ class ApproxIndex:
         torch = self._torch
         t, dt = self._xy(xy)
         n = int(t.shape[0])
-        if self._hot is None and self.n_regions > self.HOT_THRESHOLD and self.layout != "keys":
+        if self._hot is None and self.n_regions > self.HOT_THRESHOLD:
             self.auto_hot(t)
         a = None
         if attr is not None:
@@ -166,7 +166,7 @@ class ApproxIndex:
     def join_host(self, xy: np.ndarray, attr: np.ndarray | None = None):
         """rb_join_host: host (ideally pinned) buffers in, host results out."""
         xy = np.ascontiguousarray(xy) if isinstance(xy, np.ndarray) else xy
-        if self._hot is None and self.n_regions > self.HOT_THRESHOLD and self.layout != "keys":
+        if self._hot is None and self.n_regions > self.HOT_THRESHOLD:
             step = max(1, int(xy.shape[0]) // (1 << 20))
             self.auto_hot(xy[::step])
         if isinstance(xy, np.ndarray):
