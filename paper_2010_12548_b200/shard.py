@@ -17,14 +17,15 @@ def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
     return n * rank // world, n * (rank + 1) // world
 
 
-def combine(cnt, sm, group=None):
+def combine(cnt, sm, group=None, force: bool = False):
     """In-place all-reduce (sum) of the per-region partials of every rank: ONE
     collective over a packed float64 [R, 4] buffer (alpha/beta COUNT, alpha/beta
-    SUM).  Counts stay exact in float64 below 2^53 points."""
+    SUM).  Counts stay exact in float64 below 2^53 points.  force:
+    run the collective even for a single-rank group (tests of the NCCL path)."""
     import torch
     import torch.distributed as dist
 
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+    if dist.is_available() and dist.is_initialized() and (force or dist.get_world_size(group) > 1):
         buf = torch.cat([cnt.to(torch.float64), sm], dim=1)
         dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
         cnt.copy_(buf[:, :2].to(torch.int64))
