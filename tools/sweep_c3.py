@@ -35,7 +35,7 @@ for eps in (50.0, 10.0, 4.9, 1.0, 0.5):
     grid = w.grid.with_level(level_for_bound(w.grid, eps))
     L = grid.max_level
     ref_cnt = None
-    for raster, layout in (("uniform", "dense"), ("hierarchical", "trie")):
+    for raster, layout in (("uniform", "dense"), ("hierarchical", "trie"), ("hierarchical", "keys")):
         rec = {"config": "C3", "epsilon_m": eps, "level": L, "raster": raster, "layout": layout, "points": n}
         if layout == "dense" and 4.0 ** L * 4 > DENSE_MAX_BYTES:
             rec["skipped"] = f"dense leaf grid would be {4.0 ** L * 4 / 1e9:.0f} GB"
