@@ -840,10 +840,8 @@ static int index_impl(int L, int64_t total_cells, const int32_t* cp_in, const ui
     A->T0 = 0;
     A->k = std::max(1, opts->radix_width / 2);
     A->nkeys = npos;
-    int bits = 1;
-    while (bits < 2 * L && ((int64_t)1 << bits) < 2 * std::max<int64_t>(npos, 1)) ++bits;
-    bits = std::min(bits, std::min(2 * L, 29));  // ~1 cell per bucket up to 2^28 cells (a 2 GB table)
-    bits = std::max(bits, 1);
+    int bits = 0;  // ~1 cell per bucket up to 2^28 cells (a 2 GB table); 0 bits for L = 0
+    while (bits < std::min(2 * L, 29) && ((int64_t)1 << bits) < 2 * std::max<int64_t>(npos, 1)) ++bits;
     A->kshift = 2 * L - bits;
     const int64_t nslots = ((int64_t)1 << bits) + 1;
     RB_CUDA(A->ktab.alloc(nslots * 4));

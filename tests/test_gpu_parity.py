@@ -327,3 +327,24 @@ def test_sorted_key_layout(oracle_lib, mode):
         assert torch.equal(idx.lookup(sample), trie.lookup(sample))
     rep = validate_full(idx, xy, 1.0 / (1 << 12))
     assert rep.owner_set_overflows == 0
+
+
+@pytest.mark.parametrize("L", [0, 1, 2])
+def test_sorted_key_layout_tiny_grids(oracle_lib, L):
+    """RB_LAYOUT_KEYS at L = 0..2 (a bucket table of 1..16 slots) and with no
+    owner at all, against the oracle and the radix table."""
+    torch = _gpu()
+    rng = np.random.default_rng(40 + L)
+    regions = random_polygons(9, 6)
+    grid = UNIT.with_level(L)
+    xy = rng.random((50_003, 2))
+    A, _ = oracle_approx(oracle_lib, regions, grid, 0)
+    idx = _prepared(regions, grid, 0, "keys")
+    _assert_join(idx, A, xy, rng.random(len(xy)).astype(np.float32))
+    assert torch.equal(idx.lookup(xy), _prepared(regions, grid, 0, "trie").lookup(xy))
+    from paper_2010_12548_b200.geometry import Polygon, RegionRecord
+
+    far = [RegionRecord(0, Polygon([(0.01, 0.01), (0.02, 0.01), (0.02, 0.02)]))]  # touches no sample point's cell
+    idx2 = _prepared(far, UNIT.with_level(8), 0, "keys")
+    A2, _ = oracle_approx(oracle_lib, far, UNIT.with_level(8), 0)
+    _assert_join(idx2, A2, 0.5 + 0.4 * rng.random((10_001, 2)))
