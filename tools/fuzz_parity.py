@@ -4,7 +4,7 @@ points drawn uniformly, clustered, on grid lines and on polygon vertices,
 attributes spanning many magnitudes (zero, negative, out of the fixed-point
 window).  COUNT must be bit-exact, SUM within rel 1e-6.  Prints one line per
 case and a summary; exits 1 on any mismatch.
-usage: python tools/fuzz_parity.py [cases] [seed]"""
+usage: python tools/fuzz_parity.py [cases] [seed] [kind: random|holes|tiling|big]"""
 import os
 import sys
 import time
@@ -28,12 +28,12 @@ fails = 0
 t0 = time.time()
 for c in range(cases):
     rng = np.random.default_rng(seed0 + c)
-    kind = rng.choice(["random", "holes", "tiling", "big"])
+    kind = rng.choice(["random", "holes", "tiling", "big"]) if len(sys.argv) <= 3 else sys.argv[3]
     if kind == "tiling":
         regions = W.voronoi_tiling(int(rng.integers(20, 400)), 1.0, seed=int(seed0 + c), verts=(6, 20))
         L = int(rng.integers(3, 15))
     elif kind == "big":  # region sets beyond shared memory: deep / global kernels, hot slots
-        regions = W.voronoi_tiling(int(rng.integers(2000, 4000)), 1.0, seed=int(seed0 + c), verts=(6, 14))
+        regions = W.voronoi_tiling(int(rng.integers(2000, 6000)), 1.0, seed=int(seed0 + c), verts=(6, 14))
         L = int(rng.integers(10, 15))
     else:
         regions = random_polygons(int(seed0 + c), int(rng.integers(3, 40)), holes=(kind == "holes"))
@@ -56,8 +56,13 @@ for c in range(cases):
     attr = (rng.lognormal(0, 3, len(xy)) * rng.choice([-1.0, 1.0], len(xy))).astype(np.float32)
     attr[rng.random(len(xy)) < 0.05] = 0.0
     A, _ = oracle_approx(O, regions, grid, mode)
+    hot = None
+    if kind == "big" and rng.random() < 0.5:  # an explicit hot subset: cold regions take the global REDs
+        hot = np.sort(rng.choice(p.n_regions, int(rng.integers(0, min(4095, p.n_regions))), replace=False))
     for layout in layouts:
         idx = ApproxIndex(p, grid, mode, layout=layout)
+        if hot is not None:
+            idx.set_hot(hot)
         for pts, at in ((xy, attr), (xy.astype(np.float32), None)):
             pts = np.ascontiguousarray(pts)
             try:
