@@ -2,20 +2,28 @@
 """bench.py -- points/s of the epsilon-bounded point-polygon COUNT/SUM join
 (BASELINE.json metric) on B200, plus the reference CPU path.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c4|c1] [--layout trie|dense|keys]
-  python bench.py --impl reference ...        (CPU oracle port on the host cores)
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4|c2|c1] [--layout packed|trie|dense|keys]
+  python bench.py --impl reference ...        (the reference CPU path on the host cores)
+
+Default workload: C4, the largest single-GPU config of BASELINE.json (1B f32
+points, 40,000 polygons, eps = 1 m, hierarchical raster, COUNT + SUM) on the
+epsilon-matched grid (leaf side eps/sqrt(2)) with the packed cell index.
 
 One step = one point pass over this rank's batch of synthetic points (inputs
 resident in HBM, approximation prebuilt and replicated on every GPU), plus
 one NCCL all-reduce of the per-region partials packed as float64 [R,4] when
 N > 1 (weak scaling: every rank owns its own batch, seed = 0 + rank).
-Rank 0 prints ONE JSON line.  See DESIGN.md "Measurement".
+`--gpus N` without a torchrun environment re-launches itself under
+torch.distributed.run with N ranks.  Rank 0 prints ONE JSON line.  See
+DESIGN.md "Measurement".
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
+import subprocess
 import sys
 import threading
 import time
@@ -28,46 +36,112 @@ sys.path.insert(0, ROOT)
 METRIC = "points/s for eps-bounded point-polygon COUNT/SUM join"
 CONFIGS = {
     "c1": dict(workload="C1 CPU-runnable ref: 1M uniform f64 points, 100 jittered-grid tiling polygons, eps=1e-3, "
-                        "uniform raster, COUNT", points=1_000_000, bpp=16, dtype="f64"),
+                        "uniform raster, COUNT", points=1_000_000, bpp=16, dtype="f64", agg="COUNT"),
     "c2": dict(workload="C2 city-scale: 100M f64 points (50-Gaussian mixture + 10% uniform over 40x40 km), "
                         "fare f32, 260 jittered-Voronoi tiling polygons (100-500 vertices), eps=4.9 m, "
-                        "uniform raster, COUNT + SUM(fare)", points=100_000_000, bpp=20, dtype="f64"),
+                        "uniform raster, COUNT + SUM(fare)", points=100_000_000, bpp=20, dtype="f64",
+               agg="SUM:fare"),
     "c4": dict(workload="C4 fine-polygon: 1B f32-offset points (same mixture over 100x100 km), fare f32, 40,000 "
-                        "jittered-Voronoi polygons (10-30 vertices), eps=1 m, hierarchical raster, COUNT + SUM(fare)",
-               points=1_000_000_000, bpp=12, dtype="f32->f64"),
+                        "jittered-Voronoi polygons (10-30 vertices), eps=1 m, hierarchical raster (coarse interior "
+                        "cells, eps-fine boundary cells), COUNT + SUM(fare)",
+               points=1_000_000_000, bpp=12, dtype="f32->f64", agg="SUM:fare"),
 }
 REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
            0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
            0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
-    ap.add_argument("--layout", default=None, choices=["trie", "dense", "keys"])
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--layout", default=None, choices=["trie", "dense", "keys", "packed"])
+    ap.add_argument("--grid", default="eps", choices=["eps", "ingest"], help="C4 GridConfig (workloads.c4)")
+    ap.add_argument("--root-level", type=int, default=-1)
     ap.add_argument("--points", type=int, default=None, help="override points per GPU")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    return ap.parse_args()
+    ap.add_argument("--rebuilds", type=int, default=3, help="warm rebuilds timed for build_ms (median)")
+    ap.add_argument("--spawn-check", action="store_true", help=argparse.SUPPRESS)  # tests: report ranks and exit
+    return ap.parse_args(argv)
 
 
 def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
-def workload(cfg: str, n: int, rank: int):
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def relaunch(a) -> int:
+    """`--gpus N` outside torchrun: run this script under torch.distributed.run with N ranks (one per GPU)."""
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # NCCL reports its transport / algorithm choices
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT,TUNING")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
+def workload(cfg: str, n: int, rank: int, grid: str = "eps", regions=None):
     from paper_2010_12548_b200 import workloads as W
 
     if cfg == "c1":
         return W.c1(n=n, seed=0)
     if cfg == "c2":
-        return W.c2(n=n, seed=rank, regions=W.city_regions(0))
-    return W.c4(n=n, seed=0, rank=rank)
+        return W.c2(n=n, seed=rank, regions=regions if regions is not None else W.city_regions(0))
+    return W.c4(n=n, seed=0, rank=rank, grid=grid, regions=regions)
+
+
+def config_dict(a, w, L: int, world: int) -> dict:
+    """The workload description both arms print (identical dicts: same inputs, same grid, same query)."""
+    C = CONFIGS[a.config]
+    g = w.grid
+    return {"workload": C["workload"], "points_per_gpu": int(w.n), "polygons": len(w.regions),
+            "epsilon": w.epsilon, "grid": {"origin": [g.origin.x, g.origin.y], "extent": g.extent, "max_level": L,
+                                           "leaf_side": g.extent / (1 << L),
+                                           "rule": "eps-matched (leaf side eps/sqrt(2))" if a.config == "c4" and a.grid == "eps"
+                                           else "ingest (data MBR + 1%, SPEC.md:556)"},
+            "mode": "CONSERVATIVE", "agg": C["agg"], "parallelism": f"dp{world} (points per rank, approximation "
+            "replicated, one all-reduce of the packed [R,4] f64 COUNT/SUM per step)",
+            "l2": f"inputs {w.n * C['bpp'] / 1e9:.1f} GB per pass > 126 MB L2; no flush needed"
+            if w.n * C["bpp"] > 4e8 else "inputs smaller than L2 (C1 is launch-bound)"}
+
+
+def cpu_info() -> dict:
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cores": len(os.sched_getaffinity(0)), "cpu_model": model}
+
+
+def repo_libs() -> list:
+    """Shared objects of this repository mapped into the process (evidence of what ran)."""
+    out = set()
+    try:
+        with open("/proc/self/maps") as f:
+            for line in f:
+                p = line.split()[-1]
+                if p.endswith(".so") and p.startswith(os.path.realpath(ROOT)):
+                    out.add(os.path.relpath(p, os.path.realpath(ROOT)))
+    except OSError:
+        pass
+    return sorted(out)
 
 
 def peaks():
@@ -124,16 +198,23 @@ class ClockSampler(threading.Thread):
                 "samples": len(self.samples)}
 
 
-def cpu_baseline(w, grid, mode, attr, target_s: float):
-    """The oracle port (oracle/librb_oracle.so, pthreads) on a bounded prefix."""
+def oracle_approx(w, L: int):
+    """The reference CPU path's approximation (oracle/rb_oracle.c; test infrastructure, never the product)."""
     from oracle import oracle as O
     from paper_2010_12548_b200.geometry import pack_regions
 
     O.build_lib()
     p = pack_regions(w.regions)
-    A = O.Approx((grid.origin.x, grid.origin.y, grid.extent, grid.max_level), p.vx, p.vy, p.ring_off, p.poly_ring_off,
-                 p.poly_region, p.n_regions, mode)
-    cores = len(os.sched_getaffinity(0))
+    g = w.grid
+    return O.Approx((g.origin.x, g.origin.y, g.extent, L), p.vx, p.vy, p.ring_off, p.poly_ring_off, p.poly_region,
+                    p.n_regions, 0)
+
+
+def cpu_baseline(w, L, attr, target_s: float):
+    """The oracle port (oracle/librb_oracle.so, pthreads) on a bounded prefix."""
+    A = oracle_approx(w, L)
+    ci = cpu_info()
+    cores = ci["cores"]
     cal = min(w.n, 2_000_000)
     t = time.perf_counter()
     A.join(w.xy[:cal], None if attr is None else attr[:cal], nthreads=cores)
@@ -142,7 +223,7 @@ def cpu_baseline(w, grid, mode, attr, target_s: float):
     t = time.perf_counter()
     cnt, sm = A.join(w.xy[:m], None if attr is None else attr[:m], nthreads=cores)
     dt = time.perf_counter() - t
-    return dict(value=m / dt, unit="points/s", cores=cores, kind="port",
+    return dict(value=m / dt, unit="points/s", cores=cores, cpu_model=ci["cpu_model"], kind="port",
                 sample=f"first {m} of {w.n} points of the same workload, one oracle join over {cores} threads "
                        f"({dt:.1f} s)"), (m, cnt, sm)
 
@@ -155,18 +236,21 @@ def run_ours(a):
     from paper_2010_12548_b200.engine import PassResult
     from paper_2010_12548_b200.query import AggregationQuery, PreparedJoin
     from paper_2010_12548_b200.raster import RasterMode
+    from paper_2010_12548_b200.shard import combine
 
     rank, world, local = dist_env()
+    if world != a.gpus:
+        raise SystemExit(f"bench.py: --gpus {a.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", init_method="env://", device_id=torch.device("cuda", local))
     C = CONFIGS[a.config]
     n = a.points or C["points"]
-    w = workload(a.config, n, rank)
-    layout = a.layout or ("dense" if a.config == "c1" else "trie")
-    agg = "COUNT" if a.config == "c1" else "SUM:fare"
+    w = workload(a.config, n, rank, a.grid)
+    layout = a.layout or ("dense" if a.config == "c1" else ("packed" if a.config == "c4" else "trie"))
+    agg = C["agg"]
     q = AggregationQuery(agg, w.epsilon, RasterMode.CONSERVATIVE)
-    prep = PreparedJoin(w.regions, q, w.grid, layout=layout)
+    prep = PreparedJoin(w.regions, q, w.grid, layout=layout, root_level=a.root_level)
     st = prep.stats()
     grid = prep.grid
     xy = torch.from_numpy(w.xy).cuda()
@@ -177,8 +261,6 @@ def run_ours(a):
                      torch.empty((R, 2), dtype=torch.float64, device="cuda"),
                      torch.empty(1, dtype=torch.int64, device="cuda"))
     stream = torch.cuda.current_stream()
-
-    from paper_2010_12548_b200.shard import combine
 
     def step():
         prep.index.point_pass(xy, attr, out=out)
@@ -232,61 +314,69 @@ def run_ours(a):
                        "source": os.path.relpath(prof, ROOT)}
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
-            "kernel": "k_point_pass", "kernel_ms": round(k_ms, 4),
+            "kernel": "k_point_pass (ring / deep)", "kernel_ms": round(k_ms, 4),
             "algorithmic_bytes_per_point": C["bpp"], "points_per_launch": n, "index_lookups": lookups}
-    # ---- e2e: public API on pinned host buffers (rb_join_host), every step
+    # ---- e2e: public API on pinned host buffers (rb_join_host), every step; ranks combine COUNT and SUM
     e2e = None
     if not a.no_e2e:
         xy_pin = torch.from_numpy(w.xy).pin_memory()
         at_pin = torch.from_numpy(attr_np).pin_memory() if attr_np is not None else None
-        prep.index.join_host(xy_pin, at_pin)
+
+        def e2e_step():
+            cnt_h, sum_h = prep.index.join_host(xy_pin, at_pin)
+            if world > 1:
+                ct, stt = torch.from_numpy(cnt_h).cuda(), torch.from_numpy(sum_h).cuda()
+                combine(ct, stt)
+                cnt_h, sum_h = ct.cpu().numpy(), stt.cpu().numpy()
+            return cnt_h, sum_h
+
+        e2e_step()
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         k2 = a.steps
         for _ in range(k2):
-            cnt_h, sum_h = prep.index.join_host(xy_pin, at_pin)
-            if world > 1:
-                ct = torch.from_numpy(cnt_h).cuda()
-                dist.all_reduce(ct)
-                cnt_h = ct.cpu().numpy()
+            e2e_step()
         el = time.perf_counter() - t0
         if world > 1:
             t = torch.tensor([el], dtype=torch.float64, device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             el = float(t.item())
         e2e = {"value": world * n * k2 / el, "unit": "points/s", "h2d_bytes_per_step": int(n * C["bpp"]),
-               "d2h_bytes_per_step": int(R * 32 + 8), "api": "PreparedJoin.index.join_host -> rb_join_host",
+               "d2h_bytes_per_step": int(R * 32 + 8), "api": "PreparedJoin.index.join_host -> rb_join_host "
+               "(pinned host buffers, chunked H2D overlapped with the pass, results D2H)",
                "ms_per_step": round(el / k2 * 1e3, 3)}
+        del xy_pin, at_pin
     # ---- CPU baseline + parity on the same sample (rank 0, N = 1)
     cpu = None
     parity = None
     if rank == 0 and world == 1 and not a.no_cpu:
-        cpu, (m, cnt_o, sum_o) = cpu_baseline(w, grid, 0, attr_np, a.cpu_seconds)
+        cpu, (m, cnt_o, sum_o) = cpu_baseline(w, grid.max_level, attr_np, a.cpu_seconds)
         r = prep.index.point_pass(xy[:m], attr[:m] if attr is not None else None).check()
         cnt_g = r.cnt.cpu().numpy()
         ok_c = bool(np.array_equal(cnt_g, cnt_o))
         rel = float(np.max(np.abs(r.sum.cpu().numpy() - sum_o) / np.maximum(np.abs(sum_o), 1e-30))) if attr is not None else 0.0
         parity = {"points": m, "count_bit_exact": ok_c, "sum_max_rel_err": rel}
-    # the first build of a process pays module loading and allocator growth; a warm rebuild (after the
-    # timed regions, so its teardown cannot land inside them) gives the steady-state build time
-    warm = PreparedJoin(w.regions, q, w.grid, layout=layout)
-    warm_build_ms = warm.stats()["build_ms"]
-    del warm
+    # build time: the first build of a process pays module loading and allocator growth; the median of
+    # warm rebuilds (after the timed regions, so their teardown cannot land inside them) is the steady state
+    warm_ms = []
+    for _ in range(max(a.rebuilds, 0)):
+        wb = PreparedJoin(w.regions, q, w.grid, layout=layout, root_level=a.root_level)
+        warm_ms.append(wb.stats()["build_ms"])
+        del wb
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 1), "unit": "points/s", "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": round(ms / a.steps, 4), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": C["dtype"], "data": "synthetic (seeded generators, DESIGN.md Workloads)",
-            "config": {"workload": C["workload"], "points_per_gpu": n, "polygons": len(w.regions),
-                       "epsilon": w.epsilon, "max_level": grid.max_level, "mode": "CONSERVATIVE",
-                       "index": layout, "root_level": st["root_level"], "index_bytes": st["index_bytes"],
-                       "build_ms": round(warm_build_ms, 1), "build_ms_first": round(st["build_ms"], 1), "parallelism": f"dp{world} (points sharded, "
-                       "approximation replicated, one NCCL all-reduce of the packed [R,4] f64 COUNT/SUM)",
-                       "l2": f"inputs {n * C['bpp'] / 1e9:.1f} GB per pass > 126 MB L2; no flush needed"},
+            "config": config_dict(a, w, grid.max_level, world),
+            "index": {"layout": layout, "root_level": st["root_level"], "index_bytes": st["index_bytes"],
+                      "n_nodes": st["n_nodes"], "hot_regions": None if prep.index._hot is None else len(prep.index._hot),
+                      "build_ms": round(float(np.median(warm_ms)), 1) if warm_ms else None,
+                      "build_ms_runs": [round(x, 1) for x in warm_ms], "build_ms_first": round(st["build_ms"], 1)},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-            "clocks": sampler.summary(), "parity_vs_oracle": parity,
+            "clocks": sampler.summary(), "parity_vs_oracle": parity, "libs_loaded": repo_libs(),
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -295,31 +385,33 @@ def run_ours(a):
 
 def run_reference(a):
     """The reference's CPU path = the oracle port (the reference ships no
-    implementation; oracle/rb_oracle.c restates SPEC.md), all host threads."""
+    implementation; oracle/rb_oracle.c restates SPEC.md), all host threads.
+    Nothing of the product library is loaded (libs_loaded proves it)."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
     from oracle import oracle as O
-    from paper_2010_12548_b200.geometry import pack_regions
-    from paper_2010_12548_b200.grid import level_for_bound
 
     C = CONFIGS[a.config]
     n = a.points or C["points"]
-    w = workload(a.config, n, 0)
-    L = level_for_bound(w.grid, w.epsilon)
-    grid = w.grid.with_level(L)
-    attr = w.attrs.get("fare") if a.config != "c1" else None
-    p = pack_regions(w.regions)
-    O.build_lib()
-    A = O.Approx((grid.origin.x, grid.origin.y, grid.extent, L), p.vx, p.vy, p.ring_off, p.poly_ring_off,
-                 p.poly_region, p.n_regions, 0)
-    cores = len(os.sched_getaffinity(0))
-    cal = min(n, 1_000_000)
+    # the generators are chunked (2^22 points per seeded chunk), so a prefix of whole chunks is the same
+    # points as the full batch: generate one chunk to calibrate, then only the prefix the steps use
+    chunk = 1 << 22
+    w = workload(a.config, min(n, chunk), 0, a.grid)
+    L = O.level_for_bound(w.grid.extent, w.epsilon)
+    A = oracle_approx(w, L)
+    ci = cpu_info()
+    cores = ci["cores"]
+    attr = w.attrs.get("fare") if C["agg"] != "COUNT" else None
+    cal = min(w.n, 1_000_000)
     t = time.perf_counter()
     A.join(w.xy[:cal], None if attr is None else attr[:cal], nthreads=cores)
     rate = cal / max(time.perf_counter() - t, 1e-6)
     budget = 150.0 / max(a.steps + a.warmup, 1)  # whole run ~2.5 min
     m = int(min(n, max(cal, rate * budget)))
+    if m > w.n:
+        w = workload(a.config, min(n, -(-m // chunk) * chunk), 0, a.grid, regions=w.regions)
+        attr = w.attrs.get("fare") if C["agg"] != "COUNT" else None
     xs = w.xy[:m]
     at = None if attr is None else attr[:m]
     for _ in range(a.warmup):
@@ -333,19 +425,30 @@ def run_reference(a):
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": "points/s", "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": round(el / a.steps * 1e3, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": C["dtype"], "data": "synthetic", "impl": "reference",
-        "config": {"workload": C["workload"], "points_per_gpu": n, "polygons": len(w.regions), "epsilon": w.epsilon,
-                   "max_level": L, "mode": "CONSERVATIVE"},
-        "cpu_baseline": {"value": round(value, 1), "unit": "points/s", "cores": cores, "kind": "port",
-                         "sample": sample},
+        "scaling": "weak", "vs_baseline": None, "dtype": C["dtype"],
+        "data": "synthetic (seeded generators, DESIGN.md Workloads)", "impl": "reference",
+        "config": config_dict(a, w, L, world) | {"points_per_gpu": int(n)},
+        "cpu_baseline": {"value": round(value, 1), "unit": "points/s", "cores": cores, "cpu_model": ci["cpu_model"],
+                         "kind": "port", "sample": sample},
         "e2e": {"value": round(value, 1), "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "libs_loaded": repo_libs(),
     }
     print(json.dumps(line), flush=True)
 
 
+def spawn_check(a):
+    rank, world, local = dist_env()
+    print(json.dumps({"rank": rank, "world": world, "local_rank": local, "gpus": a.gpus,
+                      "nccl_debug": os.environ.get("NCCL_DEBUG")}), flush=True)
+
+
 if __name__ == "__main__":
     args = parse()
-    if args.impl == "reference":
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args))
+    if args.spawn_check:
+        spawn_check(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

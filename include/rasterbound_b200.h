@@ -47,6 +47,10 @@ extern "C" {
 #define RB_LAYOUT_TRIE 1  /* multi-level radix table (ACT, hierarchical raster) */
 #define RB_LAYOUT_KEYS 2  /* sorted 64-bit cell keys (disjoint covering cells, leaf-level start keys)
                            with a radix table over the top key bits: radix + binary search */
+#define RB_LAYOUT_PACKED 3 /* radix table root (level root_level, default L - 5) over palette-packed
+                            leaf blocks: each 4x4-leaf block of a mixed root cell is 16 bytes (three owner
+                            values + 16 two-bit palette indices), so a lookup is one root word and, inside
+                            mixed root cells, one 16-byte block (large region sets, e.g. C4) */
 
 /* point coordinate storage */
 #define RB_XY_F64 0 /* interleaved float64 (x,y) */
@@ -54,7 +58,8 @@ extern "C" {
 
 /* owner-value encoding returned by rb_lookup (one uint32 per point):
  *   0                       no owner
- *   v in [1, 2^30)          single owner: region = (v-1)>>1, boundary = (v-1)&1
+ *   v in [1, 2^18)          single owner: region = (v-1)>>1, boundary = (v-1)&1
+ *                           (region sets are limited to n_regions < 2^17: RB_CAPACITY_ERROR beyond)
  *   RB_VALUE_LIST | off     several owners: pool[off] = k, pool[off+1..k] = (region<<1)|boundary */
 #define RB_VALUE_LIST 0x40000000u
 #define RB_VALUE_PAYLOAD 0x3fffffffu
@@ -85,7 +90,7 @@ typedef struct rb_build_opts {
   int32_t mode;        /* RB_MODE_* */
   int32_t layout;      /* RB_LAYOUT_* */
   int32_t radix_width; /* ACT bits per node: 2, 4, 8; default 8 */
-  int32_t root_level;  /* TRIE root table level; -1 = automatic */
+  int32_t root_level;  /* TRIE / PACKED root table level; -1 = automatic (PACKED: L - 5, at least 0) */
   int32_t keep_cells;  /* keep per-polygon covering cells for export */
 } rb_build_opts;
 

@@ -19,7 +19,7 @@ _STATUS = {
     -6: E.ShapeError, -7: E.UnsupportedTransform,
 }
 MODE_CONSERVATIVE, MODE_CENTER_SAMPLED = 0, 1
-LAYOUT_DENSE, LAYOUT_TRIE, LAYOUT_KEYS = 0, 1, 2
+LAYOUT_DENSE, LAYOUT_TRIE, LAYOUT_KEYS, LAYOUT_PACKED = 0, 1, 2, 3
 XY_F64, XY_F32 = 0, 1
 VALUE_LIST = 0x40000000
 CODE_MASK = 0x3FFFF

@@ -37,6 +37,14 @@ class AdaptiveCellTrie:
         return self.index.stats() if self.index is not None else {}
 
 
+def _layout_code(layout: str) -> int:
+    from .engine import LAYOUTS
+
+    if layout not in LAYOUTS:
+        raise E.ConfigError(f"unknown layout {layout!r} (dense | trie | keys | packed)")
+    return LAYOUTS[layout]
+
+
 def act_build(coverings, radix_width: int = 8, root_level: int = -1, layout: str = "trie") -> AdaptiveCellTrie:
     """insert every interior/boundary cell with its region id."""
     torch = N.require_cuda()
@@ -63,7 +71,7 @@ def act_build(coverings, radix_width: int = 8, root_level: int = -1, layout: str
     t_cov, t_lv, t_code, t_kind = d(cov, None), d(lv, None), d(code.view(np.int64), None), d(kind, None)
     t_reg = d(cov_region, None)
     g = g0.native()
-    opts = N.BuildOpts(0, {"trie": N.LAYOUT_TRIE, "dense": N.LAYOUT_DENSE}[layout], radix_width, int(root_level), 0)
+    opts = N.BuildOpts(0, _layout_code(layout), radix_width, int(root_level), 0)
     h = C.c_void_p()
     N.check(N.load().rb_index_from_cells(C.byref(g), n, t_cov.data_ptr(), t_lv.data_ptr(), t_code.data_ptr(),
                                          t_kind.data_ptr(), t_reg.data_ptr(), len(coverings), len(ids), C.byref(opts),
@@ -85,7 +93,7 @@ def _from_cells(grid: GridConfig, radix_width: int, region_ids, levels, codes, k
     t_cov, t_lv = d(cov), d(np.asarray(levels, np.uint8))
     t_code, t_kind = d(np.asarray(codes, np.uint64).view(np.int64)), d(np.asarray(kinds, np.uint8))
     t_reg = d(cov_region)
-    opts = N.BuildOpts(0, {"trie": N.LAYOUT_TRIE, "dense": N.LAYOUT_DENSE}[layout], radix_width, -1, 0)
+    opts = N.BuildOpts(0, _layout_code(layout), radix_width, -1, 0)
     h = C.c_void_p()
     N.check(N.load().rb_index_from_cells(C.byref(grid.native()), len(cov), t_cov.data_ptr(), t_lv.data_ptr(),
                                          t_code.data_ptr(), t_kind.data_ptr(), t_reg.data_ptr(), len(ids), len(ids),

@@ -37,6 +37,16 @@ static cudaError_t excl_scan_i64(const int64_t* in, int64_t* out, int64_t n, cud
   return cub::DeviceScan::ExclusiveSum(t.p, tb, in, out, n, s);
 }
 
+// in-place inclusive max-scan (run heads)
+static cudaError_t incl_max_scan_i64(int64_t* a, int64_t n, cudaStream_t s) {
+  size_t tb = 0;
+  cudaError_t e = cub::DeviceScan::InclusiveScan(nullptr, tb, a, a, cub::Max(), n, s);
+  if (e) return e;
+  DBuf t;
+  if ((e = t.alloc(tb ? tb : 1))) return e;
+  return cub::DeviceScan::InclusiveScan(t.p, tb, a, a, cub::Max(), n, s);
+}
+
 template <class T>
 static cudaError_t seg_sort_keys(T* keys, int64_t n, int64_t nseg, const int64_t* beg, const int64_t* end,
                                  cudaStream_t s) {
@@ -567,23 +577,78 @@ __global__ void k_pos_owners(Recs r, int64_t n, const int64_t* pbeg, int64_t npo
     nown[P] = c;
   }
 }
-__global__ void k_pool_size(const int64_t* nown, int64_t npos, int64_t* psz) {
-  GRID_STRIDE(P, npos) psz[P] = nown[P] > 1 ? nown[P] + 1 : 0;
+// Owner lists are shared: positions with the same owner set (e.g. every boundary leaf between regions A
+// and B) get one pool entry, so a block of the index holds few distinct owner values.  Lists are hashed,
+// sorted by hash (stable: equal hashes keep position order), and a position whose list equals the first
+// list of its hash run uses that run head's entry (a hash collision just keeps its own entry).
+__device__ inline uint32_t list_entry(const Recs& r, int64_t k) {
+  return ((uint32_t)r.region[k] << 1) | (r.kind[k] == RB_KIND_B ? 1u : 0u);
+}
+__global__ void k_list_hash(Recs r, int64_t n, const int64_t* pbeg, int64_t npos, const int64_t* nown, uint64_t* key,
+                            uint32_t* idx) {
+  GRID_STRIDE(P, npos) {
+    uint64_t h = 0x9E3779B97F4A7C15ull;
+    if (nown[P] > 1) {
+      const int64_t b = pbeg[P], e = (P + 1 < npos) ? pbeg[P + 1] : n;
+      for (int64_t k = b; k < e; ++k)
+        if (k == b || r.region[k] != r.region[k - 1]) {
+          h ^= list_entry(r, k) + 0x9E3779B97F4A7C15ull + (h << 6) + (h >> 2);
+          h *= 0xff51afd7ed558ccdull;
+        }
+      h ^= h >> 33;
+      key[P] = h >> 1;  // < 2^63: single owners (all ones) sort last
+    } else {
+      key[P] = ~0ull;
+    }
+    idx[P] = (uint32_t)P;
+  }
+}
+__global__ void k_run_head(const uint64_t* key, int64_t n, int64_t* head) {
+  GRID_STRIDE(i, n) head[i] = (i == 0 || key[i] != key[i - 1]) ? i : 0;
+}
+__device__ inline bool lists_equal(const Recs& r, int64_t n, const int64_t* pbeg, int64_t npos, int64_t P, int64_t Q) {
+  int64_t a = pbeg[P], ae = (P + 1 < npos) ? pbeg[P + 1] : n;
+  int64_t b = pbeg[Q], be = (Q + 1 < npos) ? pbeg[Q + 1] : n;
+  for (;;) {
+    while (a < ae && a > pbeg[P] && r.region[a] == r.region[a - 1]) ++a;
+    while (b < be && b > pbeg[Q] && r.region[b] == r.region[b - 1]) ++b;
+    if (a == ae || b == be) return a == ae && b == be;
+    if (list_entry(r, a) != list_entry(r, b)) return false;
+    ++a;
+    ++b;
+  }
+}
+__global__ void k_list_rep(Recs r, int64_t n, const int64_t* pbeg, int64_t npos, const int64_t* nown,
+                           const uint64_t* key, const uint32_t* idx, const int64_t* head, uint32_t* rep) {
+  GRID_STRIDE(i, npos) {
+    const uint32_t P = idx[i];
+    uint32_t q = P;
+    if (nown[P] > 1) {
+      const uint32_t H = idx[head[i]];
+      if (H != P && lists_equal(r, n, pbeg, npos, P, H)) q = H;
+    }
+    rep[P] = q;
+  }
+}
+__global__ void k_pool_size(const int64_t* nown, const uint32_t* rep, int64_t npos, int64_t* psz) {
+  GRID_STRIDE(P, npos) psz[P] = (nown[P] > 1 && rep[P] == (uint32_t)P) ? nown[P] + 1 : 0;
 }
 __global__ void k_pos_values(Recs r, int64_t n, const int64_t* pbeg, int64_t npos, const int64_t* nown,
-                             const int64_t* poff, uint32_t* pool, uint64_t* pstart, uint8_t* plevel, uint32_t* pval) {
+                             const uint32_t* rep, const int64_t* poff, uint32_t* pool, uint64_t* pstart, uint8_t* plevel,
+                             uint32_t* pval) {
   GRID_STRIDE(P, npos) {
     int64_t b = pbeg[P], e = (P + 1 < npos) ? pbeg[P + 1] : n;
     pstart[P] = r.start[b];
     plevel[P] = r.level[b];
     if (nown[P] == 1) {
       pval[P] = (uint32_t)((((uint32_t)r.region[b] << 1) | (r.kind[b] == RB_KIND_B ? 1u : 0u)) + 1u);
+    } else if (rep[P] != (uint32_t)P) {
+      pval[P] = RB_VALUE_LIST | (uint32_t)poff[rep[P]];
     } else {
       int64_t w = poff[P];
       pool[w++] = RB_POOL_COUNT_FLAG | (uint32_t)nown[P];
       for (int64_t k = b; k < e; ++k)
-        if (k == b || r.region[k] != r.region[k - 1])
-          pool[w++] = ((uint32_t)r.region[k] << 1) | (r.kind[k] == RB_KIND_B ? 1u : 0u);
+        if (k == b || r.region[k] != r.region[k - 1]) pool[w++] = list_entry(r, k);
       pval[P] = RB_VALUE_LIST | (uint32_t)poff[P];
     }
   }
@@ -705,6 +770,102 @@ __global__ void k_summary(const uint32_t* root, int T0, int S, uint16_t* out) {
   }
 }
 
+// ---- RB_LAYOUT_PACKED: palette blocks from the dense leaf nodes of the mixed root cells.
+// Node n (2^pd x 2^pd leaves, row-major u32) -> 4^(pd-2) blocks of 4x4 leaves; block j of node n is
+// pblk[n * 4^(pd-2) + j].  The 16 owner values of a block with <= 3 distinct values become a palette
+// (in order of first appearance, unused entries = p0) and 2-bit indices; otherwise an escape block.
+__device__ inline int pack_gather(const uint32_t* nodes, int64_t blk, int pd, uint32_t v[16]) {
+  const int bw = pd - 2;
+  const int64_t n = blk >> (2 * bw);
+  const uint32_t j = (uint32_t)(blk & ((1ll << (2 * bw)) - 1));
+  const uint32_t bx = j & ((1u << bw) - 1u), by = j >> bw;
+  const uint32_t* nb = nodes + (n << (2 * pd));
+  int nd = 0;
+  uint32_t d0 = 0, d1 = 0, d2 = 0;
+  for (int s = 0; s < 16; ++s) {
+    const uint32_t x = (bx << 2) | (s & 3), y = (by << 2) | (s >> 2);
+    v[s] = nb[((size_t)y << pd) | x];
+    const uint32_t q = v[s];
+    if (nd > 0 && q == d0) continue;
+    if (nd > 1 && q == d1) continue;
+    if (nd > 2 && q == d2) continue;
+    if (nd == 0) d0 = q; else if (nd == 1) d1 = q; else if (nd == 2) d2 = q;
+    ++nd;
+  }
+  return nd;
+}
+__global__ void k_pack_count(const uint32_t* nodes, int64_t nblocks, int pd, uint32_t* esc) {
+  GRID_STRIDE(b, nblocks) {
+    uint32_t v[16];
+    esc[b] = pack_gather(nodes, b, pd, v) > 3 ? 1u : 0u;
+  }
+}
+__global__ void k_pack_emit(const uint32_t* nodes, int64_t nblocks, int pd, const uint32_t* esc_off, uint4* blk,
+                            uint32_t* wide) {
+  GRID_STRIDE(b, nblocks) {
+    uint32_t v[16];
+    const int nd = pack_gather(nodes, b, pd, v);
+    if (nd > 3) {
+      const uint32_t e = esc_off[b];
+      for (int s = 0; s < 16; ++s) wide[((size_t)e << 4) + s] = v[s];
+      blk[b] = make_uint4(RB_VALUE_NODE | e, 0u, 0u, 0u);
+      continue;
+    }
+    uint32_t p[3] = {v[0], v[0], v[0]};
+    int np = 1;
+    uint32_t idx = 0;
+    for (int s = 0; s < 16; ++s) {
+      int i = 0;
+      while (i < np && p[i] != v[s]) ++i;
+      if (i == np) p[np++] = v[s];
+      idx |= (uint32_t)i << (2 * s);
+    }
+    blk[b] = make_uint4(p[0], p[1], p[2], idx);
+  }
+}
+// root slots: node pointer n -> first block of node n
+__global__ void k_pack_root(uint32_t* root, int64_t n, int pd) {
+  GRID_STRIDE(k, n) {
+    const uint32_t v = root[k];
+    if (v & RB_VALUE_NODE) root[k] = RB_VALUE_NODE | ((v & RB_VALUE_PAYLOAD) << (2 * (pd - 2)));
+  }
+}
+static cudaError_t excl_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, cudaStream_t s) {
+  size_t tb = 0;
+  cudaError_t e = cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, n, s);
+  if (e) return e;
+  DBuf t;
+  if ((e = t.alloc(tb ? tb : 1))) return e;
+  return cub::DeviceScan::ExclusiveSum(t.p, tb, in, out, n, s);
+}
+
+__global__ void k_split_off(const int64_t* soffs, int64_t n, int64_t* o2) {
+  GRID_STRIDE(k, n) o2[k] = k + 3 * soffs[k];
+}
+__global__ void k_count_multi(const int64_t* nown, int64_t n, unsigned long long* out) {
+  unsigned long long c = 0;
+  GRID_STRIDE(k, n) c += nown[k] > 1 ? 1 : 0;
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+// interior cells, boundary cells, interior leaves after expansion to level L
+__global__ void k_cell_stats(const uint8_t* level, const uint8_t* kind, int64_t n, int L, unsigned long long* out) {
+  unsigned long long ni = 0, nb = 0, uni = 0;
+  GRID_STRIDE(k, n) {
+    if (kind[k] == RB_KIND_I) { ++ni; uni += 1ull << (2 * (L - level[k])); } else ++nb;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    ni += __shfl_xor_sync(0xffffffffu, ni, o);
+    nb += __shfl_xor_sync(0xffffffffu, nb, o);
+    uni += __shfl_xor_sync(0xffffffffu, uni, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (ni) atomicAdd(out, ni);
+    if (nb) atomicAdd(out + 1, nb);
+    if (uni) atomicAdd(out + 2, uni);
+  }
+}
+
 // ---------------------------------------------------------------- driver
 struct Ctx {
   cudaStream_t s;
@@ -767,13 +928,8 @@ static int index_impl(int L, int64_t total_cells, const int32_t* cp_in, const ui
     int64_t n2 = n + 3 * nsplit;
     DBuf o2;
     RB_CUDA(o2.alloc((n + 1) * 8));
-    {
-      // o2[k] = k + 3*soffs[k]
-      std::vector<int64_t> hs(n + 1);
-      RB_CUDA(cudaMemcpy(hs.data(), soffs.p, (n + 1) * 8, cudaMemcpyDeviceToHost));
-      for (int64_t k = 0; k <= n; ++k) hs[k] = k + 3 * hs[k];
-      RB_CUDA(cudaMemcpy(o2.p, hs.data(), (n + 1) * 8, cudaMemcpyHostToDevice));
-    }
+    k_split_off<<<nblk(n + 1), 256, 0, s>>>(soffs.as<int64_t>(), n + 1, o2.as<int64_t>());  // k + 3 * splits before k
+    RB_CUDA(cudaGetLastError());
     DBuf s2, l2, r2, k2;
     RB_CUDA(s2.alloc(n2 * 8));
     RB_CUDA(l2.alloc(n2));
@@ -812,7 +968,26 @@ static int index_impl(int L, int64_t total_cells, const int32_t* cp_in, const ui
   RB_CUDA(cudaMemsetAsync(nown.p, 0, (npos + 1) * 8, s));
   RB_CUDA(cudaMemsetAsync(psz.p, 0, (npos + 1) * 8, s));
   if (npos) k_pos_owners<<<nblk(npos), 256, 0, s>>>(R, n, pb.as<int64_t>(), npos, nown.as<int64_t>());
-  if (npos) k_pool_size<<<nblk(npos), 256, 0, s>>>(nown.as<int64_t>(), npos, psz.as<int64_t>());
+  DBuf rep;
+  RB_CUDA(rep.alloc(std::max<int64_t>(npos, 1) * 4));
+  if (npos) {  // shared owner lists (identical owner sets -> one pool entry)
+    if (npos >= ((int64_t)1 << 32)) return fail(RB_CAPACITY_ERROR, "more than 2^32 indexed positions");
+    DBuf hkey, hidx, hhead;
+    RB_CUDA(hkey.alloc(npos * 8));
+    RB_CUDA(hidx.alloc(npos * 4));
+    RB_CUDA(hhead.alloc(npos * 8));
+    k_list_hash<<<nblk(npos), 256, 0, s>>>(R, n, pb.as<int64_t>(), npos, nown.as<int64_t>(), hkey.as<uint64_t>(),
+                                           hidx.as<uint32_t>());
+    RB_CUDA(cudaGetLastError());
+    RB_CUDA(radix_sort_pairs(hkey.as<uint64_t>(), hidx.as<uint32_t>(), npos, 64, s));
+    k_run_head<<<nblk(npos), 256, 0, s>>>(hkey.as<uint64_t>(), npos, hhead.as<int64_t>());
+    RB_CUDA(cudaGetLastError());
+    RB_CUDA(incl_max_scan_i64(hhead.as<int64_t>(), npos, s));
+    k_list_rep<<<nblk(npos), 256, 0, s>>>(R, n, pb.as<int64_t>(), npos, nown.as<int64_t>(), hkey.as<uint64_t>(),
+                                          hidx.as<uint32_t>(), hhead.as<int64_t>(), rep.as<uint32_t>());
+    RB_CUDA(cudaGetLastError());
+  }
+  if (npos) k_pool_size<<<nblk(npos), 256, 0, s>>>(nown.as<int64_t>(), rep.as<uint32_t>(), npos, psz.as<int64_t>());
   RB_CUDA(excl_scan_i64(psz.as<int64_t>(), poff.as<int64_t>(), npos + 1, s));
   int64_t npool = d2h(poff.as<int64_t>() + npos, s);
   if (npool >= (int64_t)RB_VALUE_PAYLOAD) return fail(RB_CAPACITY_ERROR, "owner pool exceeds 2^30 entries");
@@ -822,15 +997,16 @@ static int index_impl(int L, int64_t total_cells, const int32_t* cp_in, const ui
   RB_CUDA(plevel.alloc(std::max<int64_t>(npos, 1)));
   RB_CUDA(pval.alloc(std::max<int64_t>(npos, 1) * 4));
   if (npos) k_pos_values<<<nblk(npos), 256, 0, s>>>(R, n, pb.as<int64_t>(), npos, nown.as<int64_t>(),
-                                                    poff.as<int64_t>(), A->pool.as<uint32_t>(), pstart.as<uint64_t>(),
+                                                    rep.as<uint32_t>(), poff.as<int64_t>(), A->pool.as<uint32_t>(), pstart.as<uint64_t>(),
                                                     plevel.as<uint8_t>(), pval.as<uint32_t>());
   RB_CUDA(cudaGetLastError());
   {
-    int64_t multi = 0;
-    std::vector<int64_t> hn(npos);
-    if (npos) RB_CUDA(cudaMemcpy(hn.data(), nown.p, npos * 8, cudaMemcpyDeviceToHost));
-    for (int64_t P2 = 0; P2 < npos; ++P2) multi += hn[P2] > 1;
-    A->stats.n_multi_owner = multi;
+    DBuf cm;
+    RB_CUDA(cm.alloc(8));
+    RB_CUDA(cudaMemsetAsync(cm.p, 0, 8, s));
+    if (npos) k_count_multi<<<nblk(npos), 256, 0, s>>>(nown.as<int64_t>(), npos, cm.as<unsigned long long>());
+    RB_CUDA(cudaGetLastError());
+    A->stats.n_multi_owner = (int64_t)d2h(cm.as<unsigned long long>(), s);
     A->stats.n_positions = npos;
   }
   rs.release(); rl.release(); rr.release(); rk.release(); head.release(); hpos.release(); pb.release();
@@ -884,6 +1060,13 @@ static int index_impl(int L, int64_t total_cells, const int32_t* cp_in, const ui
     // automatic root level: a 2^12 x 2^12 root (64 MB, L2-resident) leaves one node level
     // up to L = 16 (C2: 0.503 -> 0.487 ms over T0 = 10); deeper grids keep an 8 MB root (C4)
     T0 = opts->root_level >= 0 ? std::min(opts->root_level, L) : (L <= 16 ? std::min(L, 12) : 11);
+    if (opts->layout == RB_LAYOUT_PACKED) {
+      // one level of 4x4-leaf palette blocks below the root: L - T0 in [2, 8] (<= 4096 blocks per root cell)
+      T0 = opts->root_level >= 0 ? opts->root_level : std::max(0, L - 5);
+      if (L < 2) return fail(RB_CONFIG_ERROR, "the packed layout needs max_level >= 2");
+      if (L - T0 < 2 || L - T0 > 8)
+        return fail(RB_CONFIG_ERROR, "packed layout: root_level must lie in [max_level - 8, max_level - 2]");
+    }
     int rem = L - T0;
     if (const char* e = getenv("RB_NODE_KS")) {  // experiments: explicit node split, e.g. "2,5"
       for (const char* c = e; *c;) {
@@ -896,6 +1079,7 @@ static int index_impl(int L, int64_t total_cells, const int32_t* cp_in, const ui
       }
       if (rem != 0) return fail(RB_CONFIG_ERROR, "RB_NODE_KS must split L - root_level exactly");
     }
+    if (opts->layout == RB_LAYOUT_PACKED) ks.assign(1, rem);  // the dense leaf nodes, packed below
     if (ks.empty() && rem > 0) {
       int first = rem % k ? rem % k : k;
       ks.push_back(first);
@@ -996,7 +1180,34 @@ static int index_impl(int L, int64_t total_cells, const int32_t* cp_in, const ui
     }
   }
   A->node_levels.clear();
-  for (int i = 0; i < B.nlev; ++i) {
+  if (opts->layout == RB_LAYOUT_PACKED) {
+    const int pd = L - T0;
+    const int64_t bpr = (int64_t)1 << (2 * (pd - 2));
+    const int64_t nblocks = nnodes[0] * bpr;
+    if (nblocks >= (int64_t)RB_VALUE_PAYLOAD) return fail(RB_CAPACITY_ERROR, "packed index exceeds 2^30 blocks");
+    DBuf esc, eoff;
+    RB_CUDA(esc.alloc((nblocks + 1) * 4));
+    RB_CUDA(eoff.alloc((nblocks + 1) * 4));
+    RB_CUDA(cudaMemsetAsync(esc.p, 0, (nblocks + 1) * 4, s));
+    if (nblocks) k_pack_count<<<nblk(nblocks), 256, 0, s>>>(node_bufs[0].as<uint32_t>(), nblocks, pd, esc.as<uint32_t>());
+    RB_CUDA(cudaGetLastError());
+    RB_CUDA(excl_scan_u32(esc.as<uint32_t>(), eoff.as<uint32_t>(), nblocks + 1, s));
+    const int64_t nwide = d2h(eoff.as<uint32_t>() + nblocks, s);
+    RB_CUDA(A->pblk.alloc(std::max<int64_t>(nblocks, 1) * 16));
+    RB_CUDA(A->pwide.alloc(std::max<int64_t>(nwide, 1) * 64));
+    if (nblocks)
+      k_pack_emit<<<nblk(nblocks), 256, 0, s>>>(node_bufs[0].as<uint32_t>(), nblocks, pd, eoff.as<uint32_t>(),
+                                                A->pblk.as<uint4>(), A->pwide.as<uint32_t>());
+    k_pack_root<<<nblk(A->root_entries), 256, 0, s>>>(A->root.as<uint32_t>(), A->root_entries, pd);
+    RB_CUDA(cudaGetLastError());
+    RB_CUDA(cudaStreamSynchronize(s));
+    node_bufs.clear();
+    A->pd = pd;
+    A->n_pblk = nblocks;
+    A->n_pwide = nwide;
+    node_bytes = nblocks * 16 + nwide * 64;
+  }
+  for (size_t i = 0; i < node_bufs.size(); ++i) {
     A->node_levels.push_back(ks[i]);
     A->node_bufs.push_back(std::move(node_bufs[i]));
   }
@@ -1240,19 +1451,22 @@ static int build_impl(const rb_grid* grid, const rb_polygons* P, const rb_build_
     cpl.clear(); cll.clear(); ccl.clear(); ckl.clear();
   }
   {
-    // stats: interior / boundary cells and expanded interior leaves (host reduce; build path)
-    std::vector<uint8_t> hl(total_cells), hk(total_cells);
-    if (total_cells) {
-      RB_CUDA(cudaMemcpy(hl.data(), c_level.p, total_cells, cudaMemcpyDeviceToHost));
-      RB_CUDA(cudaMemcpy(hk.data(), c_kind.p, total_cells, cudaMemcpyDeviceToHost));
-    }
-    int64_t uni = 0;
-    for (int64_t k = 0; k < total_cells; ++k) {
-      if (hk[k] == RB_KIND_I) { ++n_int; uni += (int64_t)1 << (2 * (L - hl[k])); } else ++n_bnd;
-    }
+    // stats: interior / boundary cells and expanded interior leaves (device reduce)
+    DBuf cs3;
+    RB_CUDA(cs3.alloc(24));
+    RB_CUDA(cudaMemsetAsync(cs3.p, 0, 24, s));
+    if (total_cells)
+      k_cell_stats<<<nblk(total_cells), 256, 0, s>>>(c_level.as<uint8_t>(), c_kind.as<uint8_t>(), total_cells, L,
+                                                     cs3.as<unsigned long long>());
+    RB_CUDA(cudaGetLastError());
+    unsigned long long h3[3] = {0, 0, 0};
+    RB_CUDA(cudaMemcpyAsync(h3, cs3.p, 24, cudaMemcpyDeviceToHost, s));
+    RB_CUDA(cudaStreamSynchronize(s));
+    n_int = (int64_t)h3[0];
+    n_bnd = (int64_t)h3[1];
     A->stats.n_interior_cells = n_int;
     A->stats.n_boundary_cells = n_bnd;
-    A->stats.n_uniform_interior = uni;
+    A->stats.n_uniform_interior = (int64_t)h3[2];
   }
 
   int ist = index_impl(L, total_cells, c_poly.as<int32_t>(), c_level.as<uint8_t>(), c_code.as<uint64_t>(),
@@ -1284,11 +1498,13 @@ extern "C" int rb_approx_build(const rb_grid* grid, const rb_polygons* polys, co
     return fail(RB_CONFIG_ERROR, "grid extent must be finite and > 0");
   if (opts->mode != RB_MODE_CONSERVATIVE && opts->mode != RB_MODE_CENTER_SAMPLED)
     return fail(RB_CONFIG_ERROR, "unknown raster mode");
-  if (opts->layout != RB_LAYOUT_DENSE && opts->layout != RB_LAYOUT_TRIE && opts->layout != RB_LAYOUT_KEYS)
+  if (opts->layout != RB_LAYOUT_DENSE && opts->layout != RB_LAYOUT_TRIE && opts->layout != RB_LAYOUT_KEYS &&
+      opts->layout != RB_LAYOUT_PACKED)
     return fail(RB_CONFIG_ERROR, "unknown layout");
   if (opts->radix_width != 2 && opts->radix_width != 4 && opts->radix_width != 8)
     return fail(RB_CONFIG_ERROR, "radix_width must be 2, 4 or 8 (SPEC.md:278)");
-  if (polys->n_regions <= 0 || polys->n_regions >= (1 << 29)) return fail(RB_CAPACITY_ERROR, "n_regions outside [1, 2^29)");
+  if (polys->n_regions <= 0 || polys->n_regions >= RB_MAX_REGIONS)  // the 18-bit code field of owner values
+    return fail(RB_CAPACITY_ERROR, "n_regions outside [1, 2^17)");
   if (polys->n_polygons < 0 || polys->n_rings < 0 || polys->n_vertices < 0) return fail(RB_CONFIG_ERROR, "negative sizes");
   if (polys->n_polygons >= ((int64_t)1 << 31)) return fail(RB_CAPACITY_ERROR, "too many polygons");
   std::unique_ptr<rb_approx> A(new rb_approx());
@@ -1296,8 +1512,14 @@ extern "C" int rb_approx_build(const rb_grid* grid, const rb_polygons* polys, co
   A->opts = *opts;
   A->n_regions = polys->n_regions;
   A->n_polygons = polys->n_polygons;
-  int st = build_impl(grid, polys, opts, (cudaStream_t)stream, A.get());
+  int st;
+  {
+    AllocScope scope((cudaStream_t)stream);  // stream-ordered scratch from the private pool
+    st = build_impl(grid, polys, opts, (cudaStream_t)stream, A.get());
+    if (st == RB_OK) st = cudaStreamSynchronize((cudaStream_t)stream) ? cuda_fail(cudaGetLastError(), "build") : RB_OK;
+  }
   if (st != RB_OK) return st;
+  A->detach_all();
   *out = A.release();
   return RB_OK;
 }
@@ -1322,13 +1544,16 @@ extern "C" int rb_index_from_cells(const rb_grid* grid, int64_t n_cells, const i
   if (!grid || !opts || !out) return fail(RB_CONFIG_ERROR, "null argument");
   *out = nullptr;
   if (grid->max_level < 0 || grid->max_level > 31) return fail(RB_CAPACITY_ERROR, "max_level outside [0, 31]");
-  if (opts->layout != RB_LAYOUT_DENSE && opts->layout != RB_LAYOUT_TRIE && opts->layout != RB_LAYOUT_KEYS)
+  if (opts->layout != RB_LAYOUT_DENSE && opts->layout != RB_LAYOUT_TRIE && opts->layout != RB_LAYOUT_KEYS &&
+      opts->layout != RB_LAYOUT_PACKED)
     return fail(RB_CONFIG_ERROR, "unknown layout");
   if (opts->radix_width != 2 && opts->radix_width != 4 && opts->radix_width != 8)
     return fail(RB_CONFIG_ERROR, "radix_width must be 2, 4 or 8 (SPEC.md:278)");
-  if (n_regions <= 0 || n_regions >= (1 << 29)) return fail(RB_CAPACITY_ERROR, "n_regions outside [1, 2^29)");
+  if (n_regions <= 0 || n_regions >= RB_MAX_REGIONS)  // the 18-bit code field of owner values
+    return fail(RB_CAPACITY_ERROR, "n_regions outside [1, 2^17)");
   if (n_cells < 0 || n_cov < 0) return fail(RB_SHAPE_ERROR, "negative sizes");
   cudaStream_t s = (cudaStream_t)stream;
+  AllocScope scope(s);
   auto t_start = std::chrono::steady_clock::now();
   {
     std::vector<int32_t> hr(n_cov);
@@ -1358,7 +1583,9 @@ extern "C" int rb_index_from_cells(const rb_grid* grid, int64_t n_cells, const i
   A->stats.n_regions = n_regions;
   int st = index_impl(L, n_cells, cov, level, code, kind, cov_region, opts, s, A.get());
   if (st != RB_OK) return st;
+  RB_CUDA(cudaStreamSynchronize(s));
   A->stats.build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+  A->detach_all();
   *out = A.release();
   return RB_OK;
 }
@@ -1375,6 +1602,21 @@ __global__ void k_hot_values(uint32_t* v, int64_t n, const int32_t* remap) {
     const uint32_t code = x & RB_CODE_MASK;
     const uint32_t r = (code - 1u) >> 1;
     v[k] = code | ((uint32_t)remap[r] << RB_HOT_SHIFT);
+  }
+}
+__device__ __forceinline__ uint32_t hot_value(uint32_t x, const int32_t* remap) {
+  if (x == 0u || (x & (RB_VALUE_NODE | RB_VALUE_LIST))) return x;
+  const uint32_t code = x & RB_CODE_MASK;
+  return code | ((uint32_t)remap[(code - 1u) >> 1] << RB_HOT_SHIFT);
+}
+// RB_LAYOUT_PACKED: the three palette entries of every block (escape pointers are left alone)
+__global__ void k_hot_blocks(uint4* blk, int64_t n, const int32_t* remap) {
+  GRID_STRIDE(k, n) {
+    uint4 b = blk[k];
+    b.x = hot_value(b.x, remap);
+    b.y = hot_value(b.y, remap);
+    b.z = hot_value(b.z, remap);
+    blk[k] = b;
   }
 }
 // RB_LAYOUT_KEYS: annotate the single owner values of the cell records
@@ -1409,6 +1651,7 @@ extern "C" int rb_approx_set_hot(rb_approx* a, const int32_t* regions, int32_t n
   if ((int64_t)a->n_regions >= ((int64_t)1 << 17) - 1) return fail(RB_CAPACITY_ERROR, "hot slots need < 2^17 regions");
   if (n_hot == 0) return RB_OK;
   cudaStream_t s = (cudaStream_t)stream;
+  AllocScope scope(s);
   std::vector<int32_t> h(n_hot);
   RB_CUDA(cudaMemcpyAsync(h.data(), regions, n_hot * 4, cudaMemcpyDefault, s));
   RB_CUDA(cudaStreamSynchronize(s));
@@ -1430,6 +1673,9 @@ extern "C" int rb_approx_set_hot(rb_approx* a, const int32_t* regions, int32_t n
     const int64_t n = (int64_t)(a->node_bufs[i].bytes / 4);
     k_hot_values<<<nblk(n), 256, 0, s>>>(a->node_bufs[i].as<uint32_t>(), n, remap.as<int32_t>());
   }
+  if (a->n_pblk) k_hot_blocks<<<nblk(a->n_pblk), 256, 0, s>>>(a->pblk.as<uint4>(), a->n_pblk, remap.as<int32_t>());
+  if (a->n_pwide)
+    k_hot_values<<<nblk(a->n_pwide * 16), 256, 0, s>>>(a->pwide.as<uint32_t>(), a->n_pwide * 16, remap.as<int32_t>());
   if (a->pool_len) k_hot_pool<<<nblk(a->pool_len), 256, 0, s>>>(a->pool.as<uint32_t>(), a->pool_len, remap.as<int32_t>());
   RB_CUDA(cudaGetLastError());
   if (a->keys.p && a->nkeys)
@@ -1442,6 +1688,7 @@ extern "C" int rb_approx_set_hot(rb_approx* a, const int32_t* regions, int32_t n
                                                                  a->summary.as<uint16_t>());
   RB_CUDA(cudaGetLastError());
   RB_CUDA(cudaStreamSynchronize(s));
+  a->hot_region.detach();
   a->n_hot = n_hot;
   return RB_OK;
 }

@@ -304,7 +304,7 @@ extern "C" int rb_canvas_render_points(const rb_lps* lps, rb_canvas_desc* out, v
                        out->x0 + W <= ((int64_t)1 << L) && out->y0 + W <= ((int64_t)1 << L);
   if (n && aligned) {  // only the tile's slice of the sorted codes
     int64_t* range = nullptr;
-    RB_CUDA(cudaMallocAsync(&range, 16, s));
+    RB_CUDA(pool_alloc(&range, 16, s));
     k_tile_range<<<1, 1, 0, s>>>(codes, n, out->x0, out->y0, out->level, range);
     k_render_points_range<<<cb(std::min<int64_t>(n, (int64_t)npx(out) * 4)), 256, 0, s>>>(
         codes, n, range, prefix, out->n_sum, L, out->x0, out->y0, out->level, out->count, out->sums);
@@ -380,8 +380,8 @@ extern "C" int rb_canvas_reduce(const rb_canvas_desc* a, int64_t* cnt_out, doubl
   cudaStream_t s = (cudaStream_t)stream;
   long long* pc = nullptr;
   double* ps = nullptr;  // stream-ordered scratch: no host synchronisation
-  RB_CUDA(cudaMallocAsync(&pc, RB_RED_BLOCKS * 16, s));
-  RB_CUDA(cudaMallocAsync(&ps, (size_t)std::max(a->n_sum, 1) * RB_RED_BLOCKS * 16, s));
+  RB_CUDA(pool_alloc(&pc, RB_RED_BLOCKS * 16, s));
+  RB_CUDA(pool_alloc(&ps, (size_t)std::max(a->n_sum, 1) * RB_RED_BLOCKS * 16, s));
   k_reduce_px<<<RB_RED_BLOCKS, 256, 0, s>>>(npx(a), a->n_sum, a->count, a->sums, a->flags, pc, ps);
   k_reduce_px2<<<1, 32, 0, s>>>(RB_RED_BLOCKS, a->n_sum, pc, ps, cnt_out, sum_out);
   RB_CUDA(cudaGetLastError());

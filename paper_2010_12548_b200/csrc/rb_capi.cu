@@ -14,6 +14,39 @@ namespace rb {
 static thread_local std::string g_err;
 
 void set_error(const std::string& msg) { g_err = msg; }
+
+cudaStream_t& alloc_stream_tls() {
+  static thread_local cudaStream_t s = nullptr;
+  return s;
+}
+bool& alloc_scope_tls() {
+  static thread_local bool on = false;
+  return on;
+}
+cudaMemPool_t mem_pool() {
+  static std::mutex mu;
+  static cudaMemPool_t pools[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if (!pools[dev & 63]) {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t p = nullptr;
+    if (cudaMemPoolCreate(&p, &props) != cudaSuccess) {
+      cudaDeviceGetDefaultMemPool(&p, dev);  // (never expected) the device pool, attributes untouched
+    } else {
+      size_t fr = 0, tot = 0;
+      cudaMemGetInfo(&fr, &tot);
+      uint64_t thr = tot / 4;  // cache up to a quarter of the device between builds / passes
+      cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    pools[dev & 63] = p;
+  }
+  return pools[dev & 63];
+}
 int fail(int status, const std::string& msg) {
   g_err = msg;
   return status;
@@ -183,25 +216,12 @@ extern "C" int rb_exact_distance(const rb_polygons* polys, const double* px, con
 // point pass of chunk i on the compute stream (double-buffered device
 // chunks); pinned host inputs are copied directly, pageable ones are staged
 // through pinned buffers by the CUDA driver.
-static void keep_pool_warm() {
-  static std::once_flag once;
-  std::call_once(once, [] {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t thr = UINT64_MAX;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-  });
-}
 
 extern "C" int rb_join_host(const rb_approx* a, const void* xy_host, int32_t xy_dtype, int64_t n,
                             const float* attr_host, int64_t* cnt_host, double* sum_host, int64_t* first_bad_host) {
   int st = check_xy(a, xy_dtype, n);
   if (st) return st;
   if (!cnt_host || !sum_host || !first_bad_host) return fail(RB_CONFIG_ERROR, "null output buffer");
-  keep_pool_warm();
   const int R2 = 2 * a->n_regions;
   const size_t pt_bytes = xy_dtype == RB_XY_F64 ? 16 : 8;
   const int64_t chunk = std::min<int64_t>(std::max<int64_t>(n, 1), (int64_t)1 << 23);
@@ -219,10 +239,10 @@ extern "C" int rb_join_host(const rb_approx* a, const void* xy_host, int32_t xy_
   for (int i = 0; i < 2; ++i) {
     JH(cudaEventCreateWithFlags(&copied[i], cudaEventDisableTiming));
     JH(cudaEventCreateWithFlags(&consumed[i], cudaEventDisableTiming));
-    JH(cudaMallocAsync(&dxy[i], chunk * pt_bytes, cs));
-    if (attr_host) JH(cudaMallocAsync(&dat[i], chunk * 4, cs));
+    JH(pool_alloc(&dxy[i], chunk * pt_bytes, cs));
+    if (attr_host) JH(pool_alloc(&dat[i], chunk * 4, cs));
   }
-  JH(cudaMallocAsync(&dout, (size_t)std::max(R2, 1) * 16 + 8, ks));
+  JH(pool_alloc(&dout, (size_t)std::max(R2, 1) * 16 + 8, ks));
   {
     int64_t* dcnt = (int64_t*)dout;
     double* dsum = (double*)((char*)dout + (size_t)std::max(R2, 1) * 8);

@@ -27,6 +27,8 @@
 #define RB_CODE_MASK 0x3ffffu
 #define RB_POOL_COUNT_FLAG 0x80000000u
 #define RB_MAX_HOT 4095
+// single owner codes ((region << 1) | boundary) + 1 must fit RB_CODE_MASK
+#define RB_MAX_REGIONS (1 << 17)
 
 namespace rb {
 
@@ -159,18 +161,68 @@ __device__ inline double dist_rings(const double* X, const double* Y, const int6
   return best;
 }
 
-// ----------------------------------------------------------- device buffer
+// ----------------------------------------------------------- device memory
+// The library's private stream-ordered pool (one per device; freed blocks stay cached up to a release
+// threshold, so repeated builds and point passes do not pay cudaMalloc / cudaFree -- which synchronise
+// the device -- and the process-wide default pool is left alone).
+cudaMemPool_t mem_pool();
+template <class T>
+inline cudaError_t pool_alloc(T** p, size_t bytes, cudaStream_t s) {
+  return cudaMallocFromPoolAsync((void**)p, bytes ? bytes : 1, mem_pool(), s);
+}
+// Build-time allocation scope: while alive on this thread, DBuf allocations are stream-ordered on `s`
+// from the private pool (temporaries are freed stream-ordered; buffers kept by an rb_approx are
+// detached at the end of the build and later freed with cudaFree, which orders itself).
+cudaStream_t& alloc_stream_tls();
+bool& alloc_scope_tls();
+struct AllocScope {
+  cudaStream_t prev_s;
+  bool prev_on;
+  explicit AllocScope(cudaStream_t s) : prev_s(alloc_stream_tls()), prev_on(alloc_scope_tls()) {
+    alloc_stream_tls() = s;
+    alloc_scope_tls() = true;
+  }
+  ~AllocScope() {
+    alloc_stream_tls() = prev_s;
+    alloc_scope_tls() = prev_on;
+  }
+};
 struct DBuf {
   void* p = nullptr;
   size_t bytes = 0;
+  cudaStream_t s = nullptr;
+  bool pooled = false;  // stream-ordered: freed with cudaFreeAsync on `s` until detached
   DBuf() = default;
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
-  DBuf(DBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
-  DBuf& operator=(DBuf&& o) noexcept { release(); p = o.p; bytes = o.bytes; o.p = nullptr; o.bytes = 0; return *this; }
+  DBuf(DBuf&& o) noexcept : p(o.p), bytes(o.bytes), s(o.s), pooled(o.pooled) { o.p = nullptr; o.bytes = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    release();
+    p = o.p; bytes = o.bytes; s = o.s; pooled = o.pooled;
+    o.p = nullptr; o.bytes = 0;
+    return *this;
+  }
   ~DBuf() { release(); }
-  void release() { if (p) cudaFree(p); p = nullptr; bytes = 0; }
-  cudaError_t alloc(size_t b) { release(); bytes = b; return b ? cudaMalloc(&p, b) : cudaSuccess; }
+  void release() {
+    if (p) {
+      if (pooled) cudaFreeAsync(p, s); else cudaFree(p);
+    }
+    p = nullptr;
+    bytes = 0;
+  }
+  cudaError_t alloc(size_t b) {
+    release();
+    bytes = b;
+    if (!b) return cudaSuccess;
+    if (alloc_scope_tls()) {
+      s = alloc_stream_tls();
+      pooled = true;
+      return pool_alloc(&p, b, s);
+    }
+    pooled = false;
+    return cudaMalloc(&p, b);
+  }
+  void detach() { pooled = false; }  // outlives the allocating stream: cudaFree later (synchronising)
   template <class T> T* as() const { return (T*)p; }
 };
 
@@ -194,7 +246,26 @@ struct IndexView {
   const uint32_t* ktab;
   int64_t nkeys;
   int kshift;
+  // RB_LAYOUT_PACKED: root slot = owner value, or RB_VALUE_NODE | b: the root cell's 4^(pd-2) blocks of
+  // 4x4 leaves start at pblk[b] (row-major over the cell's 2^(pd-2) x 2^(pd-2) blocks, pd = L - T0).
+  // Block {p0, p1, p2, idx}: leaf s = (y & 3) * 4 + (x & 3) owns p[(idx >> 2s) & 3]; a block with more
+  // than three distinct owner values has p0 = RB_VALUE_NODE | e, idx = 0: its 16 values are pwide[16e..]
+  const uint4* pblk;
+  const uint32_t* pwide;
+  int pd;
 };
+
+// RB_LAYOUT_PACKED helpers: the block of leaf (ix, iy) in the root cell whose first block is b, and the
+// owner value of the leaf in a loaded block (escape blocks resolved with one more load)
+__device__ __forceinline__ uint32_t packed_block(uint32_t b, uint32_t ix, uint32_t iy, int pd) {
+  const uint32_t bm = (1u << (pd - 2)) - 1u;
+  return b + ((((iy >> 2) & bm) << (pd - 2)) | ((ix >> 2) & bm));
+}
+__device__ __forceinline__ uint32_t packed_slot(uint32_t ix, uint32_t iy) { return ((iy & 3u) << 2) | (ix & 3u); }
+__device__ __forceinline__ uint32_t packed_pick(const uint4& k, uint32_t s) {
+  const uint32_t i = (k.w >> (2u * s)) & 3u;
+  return i == 0u ? k.x : (i == 1u ? k.y : k.z);
+}
 
 __device__ __forceinline__ uint64_t spread_bits(uint32_t v) {
   uint64_t x = v;
@@ -249,6 +320,14 @@ __device__ __forceinline__ uint32_t index_lookup(const IndexView& v, uint32_t ix
   if (v.krec) return keys_lookup(v, ix, iy);
   int s = v.L - v.T0;
   uint32_t val = __ldg(&v.root[((size_t)(iy >> s) << v.T0) | (ix >> s)]);
+  if (v.pblk) {
+    if (val & RB_VALUE_NODE) {
+      const uint32_t sl = packed_slot(ix, iy);
+      val = packed_pick(__ldg(v.pblk + packed_block(val & RB_VALUE_PAYLOAD, ix, iy, v.pd)), sl);
+      if (val & RB_VALUE_NODE) val = __ldg(v.pwide + (((size_t)(val & RB_VALUE_PAYLOAD)) << 4) + sl);
+    }
+    return val;
+  }
 #pragma unroll
   for (int li = 0; li < RB_MAX_NODE_LEVELS; ++li) {
     if (!(val & RB_VALUE_NODE)) break;
@@ -279,6 +358,9 @@ struct rb_approx {
   rb::DBuf keys, ktab;  // RB_LAYOUT_KEYS: uint4 records (start key, owner value, level), radix table
   int64_t nkeys = 0;
   int kshift = 0;
+  rb::DBuf pblk, pwide;  // RB_LAYOUT_PACKED: palette blocks (uint4) and escape blocks (16 x u32)
+  int64_t n_pblk = 0, n_pwide = 0;
+  int pd = 0;
   rb::DBuf hot_region;  // int32 [n_hot]: hot slot -> region
   int32_t n_hot = 0;
   // optional exports
@@ -287,6 +369,14 @@ struct rb_approx {
   rb::DBuf part_poly, part_code, part_kept;
   int64_t n_partial = 0;
   rb_stats stats{};
+  // buffers kept past the build no longer belong to the build stream
+  void detach_all() {
+    for (rb::DBuf* b : {&root, &pool, &summary, &keys, &ktab, &pblk, &pwide, &hot_region, &cell_poly, &cell_level,
+                        &cell_code, &cell_kind, &part_poly, &part_code, &part_kept})
+      b->detach();
+    for (auto& b : node_bufs) b.detach();
+  }
+  ~rb_approx() { cudaDeviceSynchronize(); }  // no pass may still read the index when it is freed
   rb::IndexView view() const {
     rb::IndexView v{};
     v.root = root.as<uint32_t>();
@@ -302,6 +392,9 @@ struct rb_approx {
     v.ktab = ktab.as<uint32_t>();
     v.nkeys = nkeys;
     v.kshift = kshift;
+    v.pblk = pblk.as<uint4>();
+    v.pwide = pwide.as<uint32_t>();
+    v.pd = pd;
     return v;
   }
 };

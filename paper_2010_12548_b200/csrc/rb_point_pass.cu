@@ -324,6 +324,17 @@ __device__ __forceinline__ uint32_t ldg_pred(const uint32_t* ptr, bool pred, uin
   return v;
 }
 
+// predicated 16-byte read-only load (RB_LAYOUT_PACKED block): {dflt, 0, 0, 0} when !pred, which
+// packed_pick resolves to dflt (palette index 0)
+__device__ __forceinline__ uint4 ldg4_pred(const uint4* ptr, bool pred, uint32_t dflt) {
+  uint4 v;
+  asm("{\n .reg .pred p;\n setp.ne.u32 p, %4, 0;\n mov.u32 %0, %5;\n mov.u32 %1, 0;\n mov.u32 %2, 0;\n"
+      " mov.u32 %3, 0;\n @p ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%6];\n}\n"
+      : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+      : "r"((uint32_t)pred), "r"(dflt), "l"(ptr));
+  return v;
+}
+
 struct PassConst {
   double ox, oy, side, inv_side, lim;
   const uint32_t* root;
@@ -952,8 +963,10 @@ __device__ __forceinline__ void add_owners_w(uint32_t bins, double* slow, const 
   }
 }
 
-template <int XY, bool ATTR, int NW, int PPT, int NST, bool KEYS = false>
+// LAY: 0 = radix table (RB_LAYOUT_TRIE / DENSE), 1 = sorted keys (RB_LAYOUT_KEYS), 2 = palette blocks (RB_LAYOUT_PACKED)
+template <int XY, bool ATTR, int NW, int PPT, int NST, int LAY = 0>
 __global__ void __launch_bounds__(NW * 32 + 32, NW <= 8 ? 2 : 1) k_point_pass_ring(PassArgs a) {
+  constexpr bool KEYS = LAY == 1, PK = LAY == 2;
   constexpr int PB = XY == 0 ? 16 : 8;
   constexpr int WT = PPT * 32;  // points per consumer warp per tile
   constexpr int TP = NW * WT;   // points per CTA tile
@@ -1100,10 +1113,14 @@ __global__ void __launch_bounds__(NW * 32 + 32, NW <= 8 ? 2 : 1) k_point_pass_ri
     __syncwarp();
   };
   uint32_t rv[PPT], bx[PPT], by[PPT], nv[PPT];
-  uint32_t hv[PPT];  // KEYS: radix bucket end (rv = bucket start, ~0u = no lookup)
+  uint32_t hv[PPT];  // KEYS: radix bucket end (rv = bucket start, ~0u = no lookup); PK: leaf slot in its block
+  uint4 pb[PPT];     // PK: the palette blocks loaded in B(k-1)
+  const uint4* __restrict__ pblk = a.V.pblk;
+  const uint32_t* __restrict__ pwide = a.V.pwide;
+  const int pd = a.V.pd;
   float w1[PPT], w2[PPT];
 #pragma unroll
-  for (int j = 0; j < PPT; ++j) { rv[j] = bx[j] = by[j] = nv[j] = 0u; w1[j] = w2[j] = 0.f; }
+  for (int j = 0; j < PPT; ++j) { rv[j] = bx[j] = by[j] = nv[j] = hv[j] = 0u; w1[j] = w2[j] = 0.f; pb[j] = make_uint4(0u, 0u, 0u, 0u); }
   int st = 0;
   uint32_t ph = 0;
   int dk = 0;
@@ -1111,6 +1128,19 @@ __global__ void __launch_bounds__(NW * 32 + 32, NW <= 8 ? 2 : 1) k_point_pass_ri
   for (int64_t k = 0; k < K + 2; ++k) {
     // ------------------------------------------------------------ C(k-2)
     if (k >= 2) {
+      if constexpr (PK) {  // palette select; escape blocks (> 3 owner values) take one more load
+        bool esc = false;
+#pragma unroll
+        for (int j = 0; j < PPT; ++j) {
+          nv[j] = packed_pick(pb[j], hv[j]);
+          esc |= (int32_t)nv[j] < 0;
+        }
+        if (__any_sync(0xffffffffu, esc)) {
+#pragma unroll
+          for (int j = 0; j < PPT; ++j)
+            nv[j] = ldg_pred(pwide + ((size_t)(nv[j] & RB_VALUE_PAYLOAD) << 4) + hv[j], (int32_t)nv[j] < 0, nv[j]);
+        }
+      }
       bool anyrare = false;
 #pragma unroll
       for (int j = 0; j < PPT; ++j) {
@@ -1169,6 +1199,16 @@ __global__ void __launch_bounds__(NW * 32 + 32, NW <= 8 ? 2 : 1) k_point_pass_ri
       }
     }
     // ------------------------------------------------------------ B(k-1)
+    if constexpr (PK) {  // the 16-byte palette block of each point in a mixed root cell
+      if (k >= 1 && k <= K) {
+#pragma unroll
+        for (int j = 0; j < PPT; ++j) {
+          w2[j] = w1[j];
+          hv[j] = packed_slot(bx[j], by[j]);
+          pb[j] = ldg4_pred(pblk + packed_block(rv[j] & RB_VALUE_PAYLOAD, bx[j], by[j], pd), (int32_t)rv[j] < 0, rv[j]);
+        }
+      }
+    } else
     if constexpr (KEYS) {  // the bucket's cell records for the bucket read in A(k-1)
       if (k >= 1 && k <= K) {
 #pragma unroll
@@ -1396,8 +1436,11 @@ __device__ __forceinline__ void redg_sum(double* p, double w, bool pred) {
                : "memory");
 }
 
-template <int XY, bool ATTR, int NW, int PPT, int NST, bool KEYS = false>
+// ABL (timing experiments only, RB_DEEP_ABLATE; results are wrong): 1 = drop cold-region REDs,
+// 2 = no palette-block loads (every point of a mixed root cell counts as hot slot 0), 4 = no root loads
+template <int XY, bool ATTR, int NW, int PPT, int NST, int LAY = 0, int ABL = 0>
 __global__ void __launch_bounds__(NW * 32 + 32, 1) k_point_pass_deep(PassArgs a) {
+  constexpr bool KEYS = LAY == 1, PK = LAY == 2;
   constexpr int PB = XY == 0 ? 16 : 8;
   constexpr int WT = PPT * 32;
   constexpr int TP = NW * WT;
@@ -1527,16 +1570,40 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) k_point_pass_deep(PassArgs a)
   };
   uint32_t rv[PPT], c1[PPT], c2[PPT], nv1[PPT], nv2[PPT];
   uint32_t hv[PPT], zh[PPT];  // KEYS: radix bucket end (~0u: answered) and the leaf code's high word (c1: low word)
+  uint4 pb[PPT];              // PK: palette blocks loaded in B1 (c2: the leaf's slot in its block)
+  const uint4* __restrict__ pblk = a.V.pblk;
+  const uint32_t* __restrict__ pwide = a.V.pwide;
+  const int pd = a.V.pd;
   float w1[PPT], w2[PPT], w3[PPT];
 #pragma unroll
-  for (int j = 0; j < PPT; ++j) { rv[j] = c1[j] = c2[j] = nv1[j] = nv2[j] = 0u; w1[j] = w2[j] = w3[j] = 0.f; }
+  for (int j = 0; j < PPT; ++j) {
+    rv[j] = c1[j] = c2[j] = nv1[j] = nv2[j] = 0u;
+    w1[j] = w2[j] = w3[j] = 0.f;
+    pb[j] = make_uint4(0u, 0u, 0u, 0u);
+  }
   int st = 0;
   uint32_t ph = 0;
   int dk = 0;
   const int64_t K = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / G + 1 : 0;
-  for (int64_t k = 0; k < K + 3; ++k) {
-    // ------------------------------------------------------------ C(k-3)
-    if (k >= 3) {
+  // PK: three stages (A, B1 = block load, C = palette select + accumulate), the others four
+  constexpr int CD = PK ? 2 : 3;
+  for (int64_t k = 0; k < K + CD; ++k) {
+    // ------------------------------------------------------------ C(k-CD)
+    if (k >= CD) {
+      if constexpr (PK) {  // palette select; escape blocks (> 3 owner values) load their leaf's value
+        bool esc = false;
+#pragma unroll
+        for (int j = 0; j < PPT; ++j) {
+          w3[j] = w2[j];
+          nv2[j] = packed_pick(pb[j], c2[j]);
+          esc |= (int32_t)nv2[j] < 0;
+        }
+        if (__any_sync(0xffffffffu, esc)) {
+#pragma unroll
+          for (int j = 0; j < PPT; ++j)
+            nv2[j] = ldg_pred(pwide + ((size_t)(nv2[j] & RB_VALUE_PAYLOAD) << 4) + c2[j], (int32_t)nv2[j] < 0, nv2[j]);
+        }
+      }
       bool anyrare = false;
 #pragma unroll
       for (int j = 0; j < PPT; ++j) {
@@ -1560,8 +1627,10 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) k_point_pass_deep(PassArgs a)
         }
         const bool cold = single & (hot == 0u);
         const uint32_t q = (v & RB_CODE_MASK) - 1u;
-        redg_count(gcnt + q, cold);
-        if (ATTR) redg_sum(gsum + q, (double)w3[j], cold);
+        if constexpr (!(ABL & 1)) {
+          redg_count(gcnt + q, cold);
+          if (ATTR) redg_sum(gsum + q, (double)w3[j], cold);
+        }
         anyrare |= !single & (v != 0u);
       }
       if (__any_sync(0xffffffffu, anyrare)) {
@@ -1598,6 +1667,8 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) k_point_pass_deep(PassArgs a)
       }
     }
     // ------------------------------------------------------------ B2(k-2): node levels 1..
+    if constexpr (PK) {  // (no second node stage: C selects from the block)
+    } else
     if constexpr (KEYS) {
       if (k >= 2 && k <= K + 1) {
 #pragma unroll
@@ -1636,6 +1707,20 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) k_point_pass_deep(PassArgs a)
       }
     }
     // ------------------------------------------------------------ B1(k-1): node level 0
+    if constexpr (PK) {  // the 16-byte palette block of each point in a mixed root cell
+      if (k >= 1 && k <= K) {
+#pragma unroll
+        for (int j = 0; j < PPT; ++j) {
+          w2[j] = w1[j];
+          const uint32_t lx = c1[j] & 0xffffu, ly = c1[j] >> 16;
+          c2[j] = packed_slot(lx, ly);
+          if constexpr (ABL & 2)
+            pb[j] = make_uint4((int32_t)rv[j] < 0 ? (1u << RB_HOT_SHIFT) | 1u : rv[j], 0u, 0u, 0u);
+          else
+            pb[j] = ldg4_pred(pblk + packed_block(rv[j] & RB_VALUE_PAYLOAD, lx, ly, pd), (int32_t)rv[j] < 0, rv[j]);
+        }
+      }
+    } else
     if constexpr (KEYS) {  // RB_LAYOUT_KEYS: the bucket's cell records
       if (k >= 1 && k <= K) {
 #pragma unroll
@@ -1741,7 +1826,10 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) k_point_pass_deep(PassArgs a)
 #pragma unroll
       for (int j = 0; j < PPT; ++j) {
         const uint32_t* rp = root + (((by[j] >> s0) << T0) | (bx[j] >> s0));
-        rv[j] = ldg_pred(rp, sv[j] == 0xffffu, sv[j]);
+        if constexpr (ABL & 4)
+          rv[j] = (1u << RB_HOT_SHIFT) | 1u + (rp == nullptr);
+        else
+          rv[j] = ldg_pred(rp, sv[j] == 0xffffu, sv[j]);
         c1[j] = (bx[j] & m0) | ((by[j] & m0) << 16);
       }
       }
@@ -1872,18 +1960,6 @@ static cudaError_t launch_a(const PassArgs& a, bool vec, int blocks, size_t smem
 
 static int g_num_sms = 0;
 
-static void pool_keep_warm() {
-  static std::once_flag once;
-  std::call_once(once, [] {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t thr = UINT64_MAX;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-  });
-}
 
 // largest region count whose histogram (28 B per bin pair entry) fits the
 // 200 KB shared-memory budget of one CTA
@@ -1957,9 +2033,9 @@ struct WarpCfg { int nw, ppt, nst; };
 // rings (0.47 ms) were slower (profiles/round1/ring_config_sweep.txt).
 static const WarpCfg kWarpCfgs[] = {{16, 4, 3}, {16, 4, 4}, {16, 4, 2}, {15, 4, 2}};
 
-template <int XY, bool ATTR, int NW, int PPT, int NST, bool KEYS = false>
+template <int XY, bool ATTR, int NW, int PPT, int NST, int LAY = 0>
 static cudaError_t warp_run(const PassArgs& a, size_t smem, cudaStream_t s, int* blocks, bool launch) {
-  auto kern = k_point_pass_ring<XY, ATTR, NW, PPT, NST, KEYS>;
+  auto kern = k_point_pass_ring<XY, ATTR, NW, PPT, NST, LAY>;
   static int cached_blocks = -1;
   static size_t cached_smem = 0;
   if (cached_blocks < 0 || cached_smem != smem) {
@@ -1981,9 +2057,9 @@ static cudaError_t warp_run(const PassArgs& a, size_t smem, cudaStream_t s, int*
   return cudaGetLastError();
 }
 
-template <int XY, bool ATTR, bool KEYS = false>
+template <int XY, bool ATTR, int LAY = 0>
 static cudaError_t warp_dispatch(int ci, const PassArgs& a, size_t smem, cudaStream_t s, int* blocks, bool launch) {
-  if constexpr (KEYS) return warp_run<XY, ATTR, 16, 4, 3, true>(a, smem, s, blocks, launch);  // the default shape only
+  if constexpr (LAY != 0) return warp_run<XY, ATTR, 16, 4, 3, LAY>(a, smem, s, blocks, launch);  // the default shape only
   switch (ci) {
     case 0: return warp_run<XY, ATTR, 16, 4, 3>(a, smem, s, blocks, launch);
     case 1: return warp_run<XY, ATTR, 16, 4, 4>(a, smem, s, blocks, launch);
@@ -1992,9 +2068,9 @@ static cudaError_t warp_dispatch(int ci, const PassArgs& a, size_t smem, cudaStr
   }
 }
 
-template <int XY, bool ATTR, int NW, int PPT, int NST, bool KEYS = false>
+template <int XY, bool ATTR, int NW, int PPT, int NST, int LAY = 0, int ABL = 0>
 static cudaError_t deep_run(const PassArgs& a, size_t smem, cudaStream_t s, int* blocks, bool launch) {
-  auto kern = k_point_pass_deep<XY, ATTR, NW, PPT, NST, KEYS>;
+  auto kern = k_point_pass_deep<XY, ATTR, NW, PPT, NST, LAY, ABL>;
   static int cached_blocks = -1;
   static size_t cached_smem = 0;
   if (cached_blocks < 0 || cached_smem != smem) {
@@ -2016,9 +2092,20 @@ static cudaError_t deep_run(const PassArgs& a, size_t smem, cudaStream_t s, int*
 // 2 copies 2.07 (less L1 for lookups in flight); 2048 hot slots 2.35, 1024 2.98 (profiles/round1/deep_sweep.txt)
 static const WarpCfg kDeepCfgs[] = {{16, 4, 3}, {16, 4, 2}, {16, 4, 4}};
 
-template <int XY, bool ATTR, bool KEYS = false>
+template <int XY, bool ATTR, int LAY = 0>
 static cudaError_t deep_dispatch(int ci, const PassArgs& a, size_t smem, cudaStream_t s, int* blocks, bool launch) {
-  if constexpr (KEYS) return deep_run<XY, ATTR, 16, 4, 3, true>(a, smem, s, blocks, launch);  // default shape only
+  if constexpr (XY == 1 && ATTR && LAY == 2) {  // timing ablations of the C4 kernel (tools/, RB_DEEP_ABLATE)
+    static int abl = -1;
+    if (abl < 0) { const char* e = getenv("RB_DEEP_ABLATE"); abl = e ? atoi(e) : 0; }
+    switch (abl) {
+      case 1: return deep_run<XY, ATTR, 16, 4, 3, LAY, 1>(a, smem, s, blocks, launch);
+      case 3: return deep_run<XY, ATTR, 16, 4, 3, LAY, 3>(a, smem, s, blocks, launch);
+      case 7: return deep_run<XY, ATTR, 16, 4, 3, LAY, 7>(a, smem, s, blocks, launch);
+      case 6: return deep_run<XY, ATTR, 16, 4, 3, LAY, 6>(a, smem, s, blocks, launch);
+      default: break;
+    }
+  }
+  if constexpr (LAY != 0) return deep_run<XY, ATTR, 16, 4, 3, LAY>(a, smem, s, blocks, launch);  // default shape only
   switch (ci) {
     case 0: return deep_run<XY, ATTR, 16, 4, 3>(a, smem, s, blocks, launch);
     case 1: return deep_run<XY, ATTR, 16, 4, 2>(a, smem, s, blocks, launch);
@@ -2036,6 +2123,18 @@ static cudaError_t deep_dispatch(int ci, const PassArgs& a, size_t smem, cudaStr
        : (attr ? (vec ? FN<1, true, true>(__VA_ARGS__) : FN<1, true, false>(__VA_ARGS__))                   \
                : (vec ? FN<1, false, true>(__VA_ARGS__) : FN<1, false, false>(__VA_ARGS__))))
 
+// dtype x attribute x layout instantiation of warp_dispatch / deep_dispatch
+#define RB_DISPATCH_LAY(FN, ...)                                                                      \
+  (dtype == RB_XY_F64                                                                                 \
+       ? (attr ? (lay == 1 ? FN<0, true, 1>(__VA_ARGS__) : lay == 2 ? FN<0, true, 2>(__VA_ARGS__)     \
+                                                                    : FN<0, true, 0>(__VA_ARGS__))    \
+               : (lay == 1 ? FN<0, false, 1>(__VA_ARGS__) : lay == 2 ? FN<0, false, 2>(__VA_ARGS__)   \
+                                                                     : FN<0, false, 0>(__VA_ARGS__))) \
+       : (attr ? (lay == 1 ? FN<1, true, 1>(__VA_ARGS__) : lay == 2 ? FN<1, true, 2>(__VA_ARGS__)     \
+                                                                    : FN<1, true, 0>(__VA_ARGS__))    \
+               : (lay == 1 ? FN<1, false, 1>(__VA_ARGS__) : lay == 2 ? FN<1, false, 2>(__VA_ARGS__)   \
+                                                                     : FN<1, false, 0>(__VA_ARGS__))))
+
 // flags: bit0 = zero the outputs first, bit1 = reset first_bad first
 int point_pass(const rb_approx* A, const void* xy, int32_t dtype, int64_t n, const float* attr, int64_t* cnt_out,
                double* sum_out, int64_t* first_bad, int flags, int64_t idx_base, cudaStream_t s) {
@@ -2048,7 +2147,6 @@ int point_pass(const rb_approx* A, const void* xy, int32_t dtype, int64_t n, con
     const char* ks = getenv("RB_KERNEL");
     g_kernel_sel = ks ? atoi(ks) : 1;
   }
-  pool_keep_warm();
   const int R2 = 2 * A->n_regions;
   PassArgs a{};
   a.V = A->view();
@@ -2082,7 +2180,9 @@ int point_pass(const rb_approx* A, const void* xy, int32_t dtype, int64_t n, con
   const bool aligned = ((uintptr_t)xy % 16 == 0) && (!attr || (uintptr_t)attr % 16 == 0);
   const bool vec = ((uintptr_t)xy % 32 == 0) && (!attr || (uintptr_t)attr % (dtype == RB_XY_F64 ? 8 : 16) == 0);
   const bool keys = A->keys.p != nullptr;  // RB_LAYOUT_KEYS: the ring kernel (KEYS) or the generic kernels
-  const bool use_tma = g_kernel_sel != 0 && aligned && !keys;
+  const bool packed = A->pblk.p != nullptr;  // RB_LAYOUT_PACKED: ring / deep kernels (PK) or the generic kernel
+  const int lay = keys ? 1 : (packed ? 2 : 0);
+  const bool use_tma = g_kernel_sel != 0 && aligned && !keys && !packed;
   // histogram placement: every bin in shared memory when it fits next to the ring
   const bool smem_hist = use_tma ? ring + all_bins + summ_bytes <= RB_SMEM_BUDGET
                                  : (size_t)R2 * (attr ? 28 : 4) <= RB_SMEM_BUDGET;
@@ -2105,8 +2205,9 @@ int point_pass(const rb_approx* A, const void* xy, int32_t dtype, int64_t n, con
     return RB_OK;
   };
   cudaError_t e = cudaSuccess;
-  const bool keys_deep = keys && g_kernel_sel != 0 && aligned && L <= 20 && g_kernel_sel != 3 && g_kernel_sel != 4;
-  if (!smem_hist && !use_tma && !keys_deep) {  // fallback for misaligned inputs with large region sets
+  const bool keys_deep = (keys || packed) && g_kernel_sel != 0 && aligned && L <= 20 && g_kernel_sel != 3 && g_kernel_sel != 4;
+  if ((!smem_hist || packed) && !use_tma && !keys_deep) {  // fallback: misaligned inputs with large region sets,
+                                                          // or the packed layout beyond the ring kernels' L <= 20
     const int blocks = g_num_sms * 4;
     if (tstart()) return RB_CUDA_ERROR;
     e = dtype == RB_XY_F64 ? launch_a<0, false>(a, vec, blocks, 0, s) : launch_a<1, false>(a, vec, blocks, 0, s);
@@ -2135,7 +2236,7 @@ int point_pass(const rb_approx* A, const void* xy, int32_t dtype, int64_t n, con
     // more L1 (carveout) than they save in RED conflicts
     for (int c = 0; c < ncfg && wci < 0; ++c) {
       if (env_ci >= 0 && c != env_ci) continue;
-      if (keys && c != 0) continue;  // the KEYS ring is instantiated for the default shape only
+      if (lay != 0 && c != 0) continue;  // the KEYS / PK rings are instantiated for the default shape only
       const WarpCfg& W = kWarpCfgs[c];
       const int wpb = attr ? 3 : 1;
       const int P = R2 * wpb + 3 + (int)((33 - (R2 * wpb + 3) % 32) % 32);  // P % 32 == 1, >= 3 pad words
@@ -2147,14 +2248,7 @@ int point_pass(const rb_approx* A, const void* xy, int32_t dtype, int64_t n, con
       }
     }
     if (wci >= 0) {
-      e = keys ? (dtype == RB_XY_F64 ? (attr ? warp_dispatch<0, true, true>(wci, a, smem, s, &blocks, false)
-                                             : warp_dispatch<0, false, true>(wci, a, smem, s, &blocks, false))
-                                     : (attr ? warp_dispatch<1, true, true>(wci, a, smem, s, &blocks, false)
-                                             : warp_dispatch<1, false, true>(wci, a, smem, s, &blocks, false)))
-               : (dtype == RB_XY_F64 ? (attr ? warp_dispatch<0, true>(wci, a, smem, s, &blocks, false)
-                                             : warp_dispatch<0, false>(wci, a, smem, s, &blocks, false))
-                                     : (attr ? warp_dispatch<1, true>(wci, a, smem, s, &blocks, false)
-                                             : warp_dispatch<1, false>(wci, a, smem, s, &blocks, false)));
+      e = RB_DISPATCH_LAY(warp_dispatch, wci, a, smem, s, &blocks, false);
       if (e) return cuda_fail(e, "k_point_pass_ring setup");
       if (blocks <= 0) wci = -1;
     }
@@ -2172,21 +2266,14 @@ int point_pass(const rb_approx* A, const void* xy, int32_t dtype, int64_t n, con
     }
     void* scratch = nullptr;
     const size_t rows = (size_t)blocks * R2;
-    RB_CUDA(cudaMallocAsync(&scratch, rows * 20 + 16, s));
+    RB_CUDA(pool_alloc(&scratch, rows * 20 + 16, s));
     a.part_acc = (long long*)scratch;
     a.part_sum = (double*)((char*)scratch + rows * 8);
     a.part_cnt = (uint32_t*)((char*)scratch + rows * 16);
     int* scale = (int*)((char*)scratch + rows * 20);
     a.scale_exp = scale;  // written by the ring kernel (CTA 0) for k_reduce_fixed
     if (tstart()) return RB_CUDA_ERROR;
-    e = keys ? (dtype == RB_XY_F64 ? (attr ? warp_dispatch<0, true, true>(wci, a, smem, s, &blocks, true)
-                                           : warp_dispatch<0, false, true>(wci, a, smem, s, &blocks, true))
-                                   : (attr ? warp_dispatch<1, true, true>(wci, a, smem, s, &blocks, true)
-                                           : warp_dispatch<1, false, true>(wci, a, smem, s, &blocks, true)))
-             : (dtype == RB_XY_F64 ? (attr ? warp_dispatch<0, true>(wci, a, smem, s, &blocks, true)
-                                           : warp_dispatch<0, false>(wci, a, smem, s, &blocks, true))
-                                   : (attr ? warp_dispatch<1, true>(wci, a, smem, s, &blocks, true)
-                                           : warp_dispatch<1, false>(wci, a, smem, s, &blocks, true)));
+    e = RB_DISPATCH_LAY(warp_dispatch, wci, a, smem, s, &blocks, true);
     if (e) return cuda_fail(e, "k_point_pass_ring");
     if (tstop()) return RB_CUDA_ERROR;
     k_reduce_fixed<<<std::max(1, (R2 + 31) / 32), 1024, 0, s>>>(a.part_cnt, a.part_acc, a.part_sum, blocks, R2,
@@ -2200,7 +2287,7 @@ int point_pass(const rb_approx* A, const void* xy, int32_t dtype, int64_t n, con
   int dci = -1;
   bool nodes32 = true;
   for (const auto& nb : A->node_bufs) nodes32 = nodes32 && (int64_t)(nb.bytes / 4) < (int64_t(1) << 32);
-  const bool deep_shape = keys || (a.V.nlev >= 1 && L - a.V.T0 <= 16 && nodes32);
+  const bool deep_shape = keys || packed || (a.V.nlev >= 1 && L - a.V.T0 <= 16 && nodes32);
   if (g_kernel_sel != 0 && aligned && !smem_hist && L <= 20 && deep_shape && g_kernel_sel != 3 && g_kernel_sel != 4) {
     static int env_dci = -2, env_dc = -2;
     if (env_dci == -2) {
@@ -2216,7 +2303,7 @@ int point_pass(const rb_approx* A, const void* xy, int32_t dtype, int64_t n, con
     const int P = NH * wpb + 3 + (int)((33 - (NH * wpb + 3) % 32) % 32);  // P % 32 == 1, >= 3 pad words
     for (int c = 0; c < ncfg && dci < 0; ++c) {
       if (env_dci >= 0 && c != env_dci) continue;
-      if (keys && c != 0) continue;  // the KEYS variant exists for the default shape only
+      if (lay != 0 && c != 0) continue;  // the KEYS / PK variants exist for the default shape only
       const WarpCfg& W = kDeepCfgs[c];
       for (int C = env_dc > 0 ? env_dc : 1; C >= 1; C >>= 1) {  // one copy: the L1 is worth more (root table)
         const size_t need = (size_t)W.nw * W.nst * W.ppt * 32 * pt_bytes + (size_t)W.nw * 512 + 32 * (attr ? 12 : 4) +
@@ -2225,14 +2312,7 @@ int point_pass(const rb_approx* A, const void* xy, int32_t dtype, int64_t n, con
       }
     }
     if (dci >= 0) {
-      e = keys ? (dtype == RB_XY_F64 ? (attr ? deep_dispatch<0, true, true>(dci, a, smem, s, &blocks, false)
-                                             : deep_dispatch<0, false, true>(dci, a, smem, s, &blocks, false))
-                                     : (attr ? deep_dispatch<1, true, true>(dci, a, smem, s, &blocks, false)
-                                             : deep_dispatch<1, false, true>(dci, a, smem, s, &blocks, false)))
-               : (dtype == RB_XY_F64 ? (attr ? deep_dispatch<0, true>(dci, a, smem, s, &blocks, false)
-                                             : deep_dispatch<0, false>(dci, a, smem, s, &blocks, false))
-                                     : (attr ? deep_dispatch<1, true>(dci, a, smem, s, &blocks, false)
-                                             : deep_dispatch<1, false>(dci, a, smem, s, &blocks, false)));
+      e = RB_DISPATCH_LAY(deep_dispatch, dci, a, smem, s, &blocks, false);
       if (e) return cuda_fail(e, "k_point_pass_deep setup");
       if (blocks <= 0) dci = -1;
     }
@@ -2244,23 +2324,16 @@ int point_pass(const rb_approx* A, const void* xy, int32_t dtype, int64_t n, con
     }
     void* scratch = nullptr;
     const size_t rows = (size_t)blocks * std::max(A->n_hot, 1);
-    RB_CUDA(cudaMallocAsync(&scratch, rows * 8 + 16, s));
+    RB_CUDA(pool_alloc(&scratch, rows * 8 + 16, s));
     a.part_acc = (long long*)scratch;
     if (tstart()) return RB_CUDA_ERROR;
-    e = keys ? (dtype == RB_XY_F64 ? (attr ? deep_dispatch<0, true, true>(dci, a, smem, s, &blocks, true)
-                                           : deep_dispatch<0, false, true>(dci, a, smem, s, &blocks, true))
-                                   : (attr ? deep_dispatch<1, true, true>(dci, a, smem, s, &blocks, true)
-                                           : deep_dispatch<1, false, true>(dci, a, smem, s, &blocks, true)))
-             : (dtype == RB_XY_F64 ? (attr ? deep_dispatch<0, true>(dci, a, smem, s, &blocks, true)
-                                           : deep_dispatch<0, false>(dci, a, smem, s, &blocks, true))
-                                   : (attr ? deep_dispatch<1, true>(dci, a, smem, s, &blocks, true)
-                                           : deep_dispatch<1, false>(dci, a, smem, s, &blocks, true)));
+    e = RB_DISPATCH_LAY(deep_dispatch, dci, a, smem, s, &blocks, true);
     if (e) return cuda_fail(e, "k_point_pass_deep");
     if (tstop()) return RB_CUDA_ERROR;
     RB_CUDA(cudaFreeAsync(scratch, s));
     return RB_OK;
   }
-  if (!smem_hist && !use_tma) {  // sorted-key layout whose deep kernel did not fit: global histogram
+  if ((!smem_hist && !use_tma) || packed) {  // keys / packed layout whose ring and deep kernels did not fit: global histogram
     if (tstart()) return RB_CUDA_ERROR;
     e = dtype == RB_XY_F64 ? launch_a<0, false>(a, vec, g_num_sms * 4, 0, s) : launch_a<1, false>(a, vec, g_num_sms * 4, 0, s);
     if (e) return cuda_fail(e, "k_point_pass_global");
@@ -2278,7 +2351,7 @@ int point_pass(const rb_approx* A, const void* xy, int32_t dtype, int64_t n, con
   void* scratch = nullptr;
   const size_t rows = smem_hist ? (size_t)blocks * R2 : (size_t)blocks * std::max(A->n_hot, 1);
   const size_t sbytes = smem_hist ? rows * (4 + 8 + 8) + 16 : rows * 8 + 16;
-  RB_CUDA(cudaMallocAsync(&scratch, sbytes, s));
+  RB_CUDA(pool_alloc(&scratch, sbytes, s));
   a.part_acc = (long long*)scratch;
   a.part_sum = smem_hist ? (double*)((char*)scratch + rows * 8) : nullptr;
   a.part_cnt = smem_hist ? (uint32_t*)((char*)scratch + rows * 16) : nullptr;
@@ -2305,6 +2378,7 @@ int point_pass(const rb_approx* A, const void* xy, int32_t dtype, int64_t n, con
 }
 #undef RB_DISPATCH_TMA
 #undef RB_DISPATCH_SYNC
+#undef RB_DISPATCH_LAY
 
 // act_lookup for a batch: owner value per point
 __global__ void k_lookup(IndexView V, double ox, double oy, double side, double inv_side, double lim, const void* xy,

@@ -509,7 +509,7 @@ struct SBuf {
   SBuf(const SBuf&) = delete;
   SBuf& operator=(const SBuf&) = delete;
   ~SBuf() { if (p) cudaFreeAsync(p, s); }
-  cudaError_t alloc(size_t b) { return cudaMallocAsync(&p, b ? b : 1, s); }
+  cudaError_t alloc(size_t b) { return pool_alloc(&p, b, s); }
   template <class T> T* as() const { return (T*)p; }
 };
 

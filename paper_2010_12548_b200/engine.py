@@ -21,7 +21,7 @@ from .geometry import DevicePolygons, PackedRegions
 from .grid import GridConfig
 
 INT64_MAX = (1 << 63) - 1
-LAYOUTS = {"dense": N.LAYOUT_DENSE, "trie": N.LAYOUT_TRIE, "keys": N.LAYOUT_KEYS}
+LAYOUTS = {"dense": N.LAYOUT_DENSE, "trie": N.LAYOUT_TRIE, "keys": N.LAYOUT_KEYS, "packed": N.LAYOUT_PACKED}
 
 
 @dataclass
@@ -44,7 +44,7 @@ class ApproxIndex:
                  stream=None):
         torch = N.require_cuda()
         if layout not in LAYOUTS:
-            raise E.ConfigError(f"unknown layout {layout!r} (dense | trie | keys)")
+            raise E.ConfigError(f"unknown layout {layout!r} (dense | trie | keys | packed)")
         self.packed = packed
         self.grid = grid
         self.mode = int(mode)

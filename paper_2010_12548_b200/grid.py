@@ -171,7 +171,28 @@ def ingest_grid(xmin: float, ymin: float, xmax: float, ymax: float, pad: float =
     return GridConfig(Point2D(xmin - pad * span, ymin - pad * span), (1.0 + 2.0 * pad) * span, 0)
 
 
+def eps_grid(xmin: float, ymin: float, xmax: float, ymax: float, epsilon: float, pad: float = 0.01) -> GridConfig:
+    """epsilon-matched GridConfig: the leaf side is exactly epsilon/sqrt(2) (the paper's "diagonal of the
+    cell is epsilon"), at the smallest level whose domain holds the data MBR padded as by the
+    ingest rule.  The ingest grid instead fixes the extent and lets level_for_bound round the
+    side down to a power-of-two fraction of it (up to 2x finer than epsilon requires).
+    level_for_bound(eps_grid(..., epsilon), epsilon) is the returned max_level."""
+    if not (epsilon > 0.0) or not math.isfinite(epsilon):
+        raise E.ConfigError("epsilon must be finite and > 0")
+    span = max(xmax - xmin, ymax - ymin)
+    if not (span > 0.0):
+        span = 1.0
+    side = epsilon / math.sqrt(2.0)  # the same IEEE expression as rb_level_for_bound
+    need = (1.0 + 2.0 * pad) * span
+    L = 0
+    while math.ldexp(side, L) < need:
+        L += 1
+        if L > 31:
+            raise E.CapacityError("epsilon requires a level above 31 (SPEC.md:129)")
+    return GridConfig(Point2D(xmin - pad * span, ymin - pad * span), math.ldexp(side, L), L)
+
+
 __all__ = [
     "GridConfig", "CellId", "CellInterval", "level_for_bound", "z_encode", "z_decode", "point_to_cell",
-    "points_to_cells", "cell_interval", "children", "parent", "ingest_grid",
+    "points_to_cells", "cell_interval", "children", "parent", "ingest_grid", "eps_grid",
 ]

@@ -29,7 +29,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from .geometry import Polygon, RegionRecord
-from .grid import GridConfig, ingest_grid
+from .grid import GridConfig, eps_grid, ingest_grid
 
 
 # ------------------------------------------------------------- validation
@@ -322,14 +322,23 @@ def fine_regions(seed: int = 0, n_polys: int = 40_000, width: float = 100_000.0)
     return voronoi_tiling(n_polys, width, seed, verts=(10, 30))
 
 
-def c4(n: int = 1_000_000_000, seed: int = 0, regions: list | None = None, rank: int = 0) -> Workload:
+def c4(n: int = 1_000_000_000, seed: int = 0, regions: list | None = None, rank: int = 0,
+       grid: str = "eps") -> Workload:
+    """grid="eps": the epsilon-matched GridConfig (leaf side exactly eps/sqrt(2) = 0.707 m, L = 18 over a
+    185 km domain holding the padded 100 km data MBR; grid.eps_grid), the north star's "cell side
+    eps/sqrt(2)".  grid="ingest": the SPEC ingest rule (102 km domain, L = 18, side 0.389 m)."""
     W = 100_000.0
+    eps = 1.0
     regions = regions if regions is not None else fine_regions(seed)
     mx = make_mixture(W, seed)
     xy = mixture_points(n, mx, seed + rank, np.float32)
     f = fares(n, seed + rank)
-    return Workload("C4", regions, xy, {"fare": f}, ingest_grid(0.0, 0.0, W, W), 1.0, "trie", "SUM:fare",
-                    {"points": n, "polygons": len(regions), "seed": seed + rank, "extent_m": W, "xy": "f32 offsets"})
+    if grid not in ("eps", "ingest"):
+        raise ValueError("grid must be 'eps' or 'ingest'")
+    g = eps_grid(0.0, 0.0, W, W, eps) if grid == "eps" else ingest_grid(0.0, 0.0, W, W)
+    return Workload("C4", regions, xy, {"fare": f}, g, eps, "packed", "SUM:fare",
+                    {"points": n, "polygons": len(regions), "seed": seed + rank, "extent_m": W, "xy": "f32 offsets",
+                     "grid": grid})
 
 
 __all__ = [
