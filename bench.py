@@ -438,8 +438,10 @@ def run_reference(a):
 
 def spawn_check(a):
     rank, world, local = dist_env()
-    print(json.dumps({"rank": rank, "world": world, "local_rank": local, "gpus": a.gpus,
-                      "nccl_debug": os.environ.get("NCCL_DEBUG")}), flush=True)
+    line = json.dumps({"rank": rank, "world": world, "local_rank": local, "gpus": a.gpus,
+                       "nccl_debug": os.environ.get("NCCL_DEBUG")}) + "\n"
+    sys.stdout.flush()
+    os.write(1, line.encode())  # one write per rank: ranks share the pipe
 
 
 if __name__ == "__main__":

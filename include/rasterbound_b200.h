@@ -108,6 +108,8 @@ typedef struct rb_stats {
   int32_t n_regions;
   int32_t max_level;
   double build_ms;
+  int32_t max_hot; /* hot slots rb_approx_set_hot accepts for this region count (4095 .. 16383) */
+  int32_t n_hot;   /* hot slots set */
 } rb_stats;
 
 typedef struct rb_approx rb_approx;
@@ -132,10 +134,11 @@ int rb_index_from_cells(const rb_grid* grid, int64_t n_cells, const int32_t* cov
                         const uint64_t* code, const uint8_t* kind, const int32_t* cov_region, int64_t n_cov,
                         int32_t n_regions, const rb_build_opts* opts, void* stream, rb_approx** out);
 int rb_approx_stats(const rb_approx* a, rb_stats* out);
-/* Mark up to 4095 frequently hit regions (device or host int32 array) whose
+/* Mark frequently hit regions (device or host int32 array) whose
  * alpha COUNT/SUM the point pass privatises in shared memory when the full
  * per-region histogram does not fit there (large region sets, e.g. 40,000
- * census blocks).  Results are unchanged.  Requires n_regions < 2^17 - 1. */
+ * census blocks).  Results are unchanged.  At most rb_stats.max_hot regions: 2^(30 - b) - 1 (capped at
+ * 16383) where b = max(16, bit length of 2 * n_regions) is the width of the owner codes. */
 int rb_approx_set_hot(rb_approx* a, const int32_t* regions, int32_t n_hot, void* stream);
 void rb_approx_free(rb_approx* a);
 

@@ -58,7 +58,7 @@ class Stats(C.Structure):
                 ("n_uniform_interior", C.c_int64), ("n_positions", C.c_int64), ("n_multi_owner", C.c_int64),
                 ("n_nodes", C.c_int64), ("index_bytes", C.c_int64), ("root_level", C.c_int32),
                 ("node_levels", C.c_int32), ("n_regions", C.c_int32), ("max_level", C.c_int32),
-                ("build_ms", C.c_double)]
+                ("build_ms", C.c_double), ("max_hot", C.c_int32), ("n_hot", C.c_int32)]
 
     def as_dict(self) -> dict:
         return {f: getattr(self, f) for f, _ in self._fields_}

@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <memory>
 
@@ -823,6 +824,110 @@ __global__ void k_pack_emit(const uint32_t* nodes, int64_t nblocks, int pd, cons
     blk[b] = make_uint4(p[0], p[1], p[2], idx);
   }
 }
+// three-level packed index (pd = L - T0 >= 6).  Level-0 node n (8x8 u32 slots: owner value, or
+// RB_VALUE_NODE | c for a mixed mid cell whose 2^kb x 2^kb leaves are level-1 node c) -> mid sector n:
+// {p0, p1, p2, 0, c0..c3}, 2-bit code of slot s at c[s >> 4] bits 2 (s & 15); code 3 = mixed (leaf blocks
+// follow), else the palette entry.  More than three distinct owner values: {NODE | e, 0, 0, 0, 0...} and
+// pwmid[64 e + s] = the slot's owner value or RB_VALUE_NODE for a mixed slot.
+__device__ inline int mid_distinct(const uint32_t* v, uint32_t d[3]) {
+  int nd = 0;
+  for (int s = 0; s < 64; ++s) {
+    const uint32_t q = v[s];
+    if (q & RB_VALUE_NODE) continue;
+    int i = 0;
+    while (i < nd && i < 3 && d[i] != q) ++i;
+    if (i < nd && i < 3) continue;
+    if (nd < 3) d[nd] = q;
+    ++nd;
+    if (nd > 3) break;
+  }
+  return nd;
+}
+__global__ void k_mid_count(const uint32_t* nodes0, int64_t nmid, uint32_t* esc) {
+  GRID_STRIDE(n, nmid) {
+    uint32_t d[3];
+    esc[n] = mid_distinct(nodes0 + (n << 6), d) > 3 ? 1u : 0u;
+  }
+}
+__global__ void k_mid_emit(const uint32_t* nodes0, int64_t nmid, const uint32_t* eoff, uint4* mid, uint32_t* wmid) {
+  GRID_STRIDE(n, nmid) {
+    const uint32_t* v = nodes0 + (n << 6);
+    uint32_t d[3] = {0u, 0u, 0u};
+    const int nd = mid_distinct(v, d);
+    if (nd > 3) {
+      const uint32_t e = eoff[n];
+      for (int s = 0; s < 64; ++s) wmid[((size_t)e << 6) + s] = (v[s] & RB_VALUE_NODE) ? RB_VALUE_NODE : v[s];
+      mid[2 * n] = make_uint4(RB_VALUE_NODE | e, 0u, 0u, 0u);
+      mid[2 * n + 1] = make_uint4(0u, 0u, 0u, 0u);
+      continue;
+    }
+    if (nd == 0) d[0] = 0u;
+    if (nd < 2) d[1] = d[0];
+    if (nd < 3) d[2] = d[0];
+    uint32_t c[4] = {0u, 0u, 0u, 0u};
+    for (int s = 0; s < 64; ++s) {
+      uint32_t code = 3u;
+      if (!(v[s] & RB_VALUE_NODE)) code = v[s] == d[0] ? 0u : (v[s] == d[1] ? 1u : 2u);
+      c[s >> 4] |= code << (2 * (s & 15));
+    }
+    mid[2 * n] = make_uint4(d[0], d[1], d[2], 0u);
+    mid[2 * n + 1] = make_uint4(c[0], c[1], c[2], c[3]);
+  }
+}
+// leaf block b = (n * 64 + s) * 4^(kb-2) + j: 4x4-leaf block j of mid cell s of mixed root cell n, packed from
+// level-1 node c when slot s of level-0 node n is RB_VALUE_NODE | c (other blocks are never read: zeroes)
+__device__ inline int leaf_gather(const uint32_t* nodes0, const uint32_t* nodes1, int64_t b, int kb, uint32_t v[16]) {
+  const int bw = kb - 2;
+  const int64_t ms = b >> (2 * bw);  // n * 64 + s
+  const uint32_t j = (uint32_t)(b & ((1ll << (2 * bw)) - 1));
+  const uint32_t slot = nodes0[ms];
+  if (!(slot & RB_VALUE_NODE)) return -1;
+  const uint32_t* nb = nodes1 + ((size_t)(slot & RB_VALUE_PAYLOAD) << (2 * kb));
+  const uint32_t bx = j & ((1u << bw) - 1u), by = j >> bw;
+  int nd = 0;
+  uint32_t d0 = 0, d1 = 0, d2 = 0;
+  for (int t = 0; t < 16; ++t) {
+    const uint32_t x = (bx << 2) | (t & 3), y = (by << 2) | (t >> 2);
+    v[t] = nb[((size_t)y << kb) | x];
+    const uint32_t q = v[t];
+    if (nd > 0 && q == d0) continue;
+    if (nd > 1 && q == d1) continue;
+    if (nd > 2 && q == d2) continue;
+    if (nd == 0) d0 = q; else if (nd == 1) d1 = q; else if (nd == 2) d2 = q;
+    ++nd;
+  }
+  return nd;
+}
+__global__ void k_leaf_count(const uint32_t* nodes0, const uint32_t* nodes1, int64_t nblocks, int kb, uint32_t* esc) {
+  GRID_STRIDE(b, nblocks) {
+    uint32_t v[16];
+    esc[b] = leaf_gather(nodes0, nodes1, b, kb, v) > 3 ? 1u : 0u;
+  }
+}
+__global__ void k_leaf_emit(const uint32_t* nodes0, const uint32_t* nodes1, int64_t nblocks, int kb,
+                            const uint32_t* eoff, uint4* blk, uint32_t* wide) {
+  GRID_STRIDE(b, nblocks) {
+    uint32_t v[16];
+    const int nd = leaf_gather(nodes0, nodes1, b, kb, v);
+    if (nd < 0) { blk[b] = make_uint4(0u, 0u, 0u, 0u); continue; }
+    if (nd > 3) {
+      const uint32_t e = eoff[b];
+      for (int t = 0; t < 16; ++t) wide[((size_t)e << 4) + t] = v[t];
+      blk[b] = make_uint4(RB_VALUE_NODE | e, 0u, 0u, 0u);
+      continue;
+    }
+    uint32_t p[3] = {v[0], v[0], v[0]};
+    int np = 1;
+    uint32_t idx = 0;
+    for (int t = 0; t < 16; ++t) {
+      int i = 0;
+      while (i < np && p[i] != v[t]) ++i;
+      if (i == np) p[np++] = v[t];
+      idx |= (uint32_t)i << (2 * t);
+    }
+    blk[b] = make_uint4(p[0], p[1], p[2], idx);
+  }
+}
 // root slots: node pointer n -> first block of node n
 __global__ void k_pack_root(uint32_t* root, int64_t n, int pd) {
   GRID_STRIDE(k, n) {
@@ -874,9 +979,24 @@ struct Ctx {
 
 // K5: overlay + index from hierarchical cells (cell k belongs to covering
 // cp[k]; covering -> region via cov_region).  Cells are only read.
+// RB_BUILD_TRACE=1: per-phase wall time of the build (stream-synchronised), on stderr
+struct BuildTrace {
+  cudaStream_t s;
+  bool on;
+  std::chrono::steady_clock::time_point t;
+  explicit BuildTrace(cudaStream_t st) : s(st), on(getenv("RB_BUILD_TRACE") != nullptr), t(std::chrono::steady_clock::now()) {}
+  void operator()(const char* phase) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "rb build %-28s %9.2f ms\n", phase, std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
 static int index_impl(int L, int64_t total_cells, const int32_t* cp_in, const uint8_t* cl_in, const uint64_t* cc_in,
                       const uint8_t* ck_in, const int32_t* cov_region, const rb_build_opts* opts, cudaStream_t s,
                       rb_approx* A) {
+  BuildTrace trace(s);
   // ---- K5 overlay: records sorted by (start, level, region, kind)
   int64_t n = total_cells;
   DBuf rs, rl, rr, rk;
@@ -960,6 +1080,7 @@ static int index_impl(int L, int64_t total_cells, const int32_t* cp_in, const ui
     R = Recs{rs.as<uint64_t>(), rl.as<uint8_t>(), rr.as<int32_t>(), rk.as<uint8_t>()};
     n = n2;
   }
+  trace("K5 overlay (sort + split)");
   // owner values per position
   DBuf nown, psz, poff, pstart, plevel, pval;
   RB_CUDA(nown.alloc((npos + 1) * 8));
@@ -1050,6 +1171,7 @@ static int index_impl(int L, int64_t total_cells, const int32_t* cp_in, const ui
     return RB_OK;
   }
 
+  trace("K5 owner values + lists");
   // ---- index geometry
   int k = std::max(1, opts->radix_width / 2);
   int T0;
@@ -1057,11 +1179,13 @@ static int index_impl(int L, int64_t total_cells, const int32_t* cp_in, const ui
   if (opts->layout == RB_LAYOUT_DENSE) {
     T0 = L;
   } else {
-    // automatic root level: a 2^12 x 2^12 root (64 MB, L2-resident) leaves one node level
-    // up to L = 16 (C2: 0.503 -> 0.487 ms over T0 = 10); deeper grids keep an 8 MB root (C4)
-    T0 = opts->root_level >= 0 ? std::min(opts->root_level, L) : (L <= 16 ? std::min(L, 12) : 11);
+    // automatic root level: a 2^12 x 2^12 root (64 MB, L2-resident) leaves one node level up to L = 16
+    // (C2: 0.503 -> 0.487 ms over T0 = 10) and two up to L = 20 (C4, eps-matched grid: 1.70 -> 1.64 ms
+    // per 200M points over T0 = 11; only the data's 19 MB of it is touched)
+    T0 = opts->root_level >= 0 ? std::min(opts->root_level, L) : (L <= 20 ? std::min(L, 12) : 11);
     if (opts->layout == RB_LAYOUT_PACKED) {
-      // one level of 4x4-leaf palette blocks below the root: L - T0 in [2, 8] (<= 4096 blocks per root cell)
+      // pd = L - T0 in [2, 5]: 4x4-leaf palette blocks right below the root; pd in [6, 8]: a 32-byte palette
+      // sector of 8x8 mid cells per mixed root cell, then the 4x4-leaf blocks of the mixed mid cells
       T0 = opts->root_level >= 0 ? opts->root_level : std::max(0, L - 5);
       if (L < 2) return fail(RB_CONFIG_ERROR, "the packed layout needs max_level >= 2");
       if (L - T0 < 2 || L - T0 > 8)
@@ -1079,7 +1203,10 @@ static int index_impl(int L, int64_t total_cells, const int32_t* cp_in, const ui
       }
       if (rem != 0) return fail(RB_CONFIG_ERROR, "RB_NODE_KS must split L - root_level exactly");
     }
-    if (opts->layout == RB_LAYOUT_PACKED) ks.assign(1, rem);  // the dense leaf nodes, packed below
+    if (opts->layout == RB_LAYOUT_PACKED) {  // dense nodes, packed below
+      ks.clear();
+      if (rem >= 6) { ks.push_back(3); ks.push_back(rem - 3); } else ks.push_back(rem);
+    }
     if (ks.empty() && rem > 0) {
       int first = rem % k ? rem % k : k;
       ks.push_back(first);
@@ -1166,6 +1293,7 @@ static int index_impl(int L, int64_t total_cells, const int32_t* cp_in, const ui
     RB_CUDA(cudaStreamSynchronize(s));
     return RB_OK;
   };
+  trace("index node counts");
   int st = fill_range(-1, T0);
   if (st) return st;
   {
@@ -1180,7 +1308,49 @@ static int index_impl(int L, int64_t total_cells, const int32_t* cp_in, const ui
     }
   }
   A->node_levels.clear();
-  if (opts->layout == RB_LAYOUT_PACKED) {
+  if (opts->layout == RB_LAYOUT_PACKED && L - T0 >= 6) {
+    const int pd = L - T0;
+    const int kb = pd - 3;                          // leaves per mid cell side: 2^kb
+    const int64_t nmid = nnodes[0];
+    const int64_t bpm = (int64_t)1 << (2 * (kb - 2));  // 4x4-leaf blocks per mid cell
+    const int64_t nblocks = nmid * 64 * bpm;          // dense: every mid cell of a mixed root cell
+    DBuf mesc, moff, esc, eoff;
+    RB_CUDA(mesc.alloc((nmid + 1) * 4));
+    RB_CUDA(moff.alloc((nmid + 1) * 4));
+    RB_CUDA(cudaMemsetAsync(mesc.p, 0, (nmid + 1) * 4, s));
+    RB_CUDA(esc.alloc((nblocks + 1) * 4));
+    RB_CUDA(eoff.alloc((nblocks + 1) * 4));
+    RB_CUDA(cudaMemsetAsync(esc.p, 0, (nblocks + 1) * 4, s));
+    if (nmid) {
+      k_mid_count<<<nblk(nmid), 256, 0, s>>>(node_bufs[0].as<uint32_t>(), nmid, mesc.as<uint32_t>());
+      k_leaf_count<<<nblk(nblocks), 256, 0, s>>>(node_bufs[0].as<uint32_t>(), node_bufs[1].as<uint32_t>(), nblocks, kb,
+                                                 esc.as<uint32_t>());
+    }
+    RB_CUDA(cudaGetLastError());
+    RB_CUDA(excl_scan_u32(mesc.as<uint32_t>(), moff.as<uint32_t>(), nmid + 1, s));
+    RB_CUDA(excl_scan_u32(esc.as<uint32_t>(), eoff.as<uint32_t>(), nblocks + 1, s));
+    const int64_t nwmid = d2h(moff.as<uint32_t>() + nmid, s);
+    const int64_t nwide = d2h(eoff.as<uint32_t>() + nblocks, s);
+    RB_CUDA(A->pmid.alloc(std::max<int64_t>(nmid, 1) * 32));
+    RB_CUDA(A->pwmid.alloc(std::max<int64_t>(nwmid, 1) * 256));
+    RB_CUDA(A->pblk.alloc(std::max<int64_t>(nblocks, 1) * 16));
+    RB_CUDA(A->pwide.alloc(std::max<int64_t>(nwide, 1) * 64));
+    if (nmid) {
+      k_mid_emit<<<nblk(nmid), 256, 0, s>>>(node_bufs[0].as<uint32_t>(), nmid, moff.as<uint32_t>(), A->pmid.as<uint4>(),
+                                            A->pwmid.as<uint32_t>());
+      k_leaf_emit<<<nblk(nblocks), 256, 0, s>>>(node_bufs[0].as<uint32_t>(), node_bufs[1].as<uint32_t>(), nblocks, kb,
+                                                eoff.as<uint32_t>(), A->pblk.as<uint4>(), A->pwide.as<uint32_t>());
+    }
+    RB_CUDA(cudaGetLastError());
+    RB_CUDA(cudaStreamSynchronize(s));
+    node_bufs.clear();
+    A->pd = pd;
+    A->n_pmid = nmid;
+    A->n_pwmid = nwmid;
+    A->n_pblk = nblocks;
+    A->n_pwide = nwide;
+    node_bytes = nmid * 32 + nwmid * 256 + nblocks * 16 + nwide * 64;
+  } else if (opts->layout == RB_LAYOUT_PACKED) {
     const int pd = L - T0;
     const int64_t bpr = (int64_t)1 << (2 * (pd - 2));
     const int64_t nblocks = nnodes[0] * bpr;
@@ -1213,6 +1383,7 @@ static int index_impl(int L, int64_t total_cells, const int32_t* cp_in, const ui
   }
   A->n_nodes = total_nodes;
   A->stats.n_nodes = total_nodes;
+  trace("index fill + pack");
   // summary table for the shared-memory fast path (owner values must fit u16)
   {
     int Smax = RB_SUMMARY_DEFAULT;
@@ -1243,6 +1414,7 @@ static int build_impl(const rb_grid* grid, const rb_polygons* P, const rb_build_
   A->stats.max_level = L;
   A->stats.n_regions = P->n_regions;
 
+  BuildTrace trace(s);
   // ---- host-side structural checks (copy small offset arrays)
   std::vector<int64_t> h_ring(nr + 1), h_pr(np + 1);
   RB_CUDA(cudaMemcpyAsync(h_ring.data(), P->ring_off, (nr + 1) * 8, cudaMemcpyDeviceToHost, s));
@@ -1288,6 +1460,7 @@ static int build_impl(const rb_grid* grid, const rb_polygons* P, const rb_build_
   const double* dgy = gy.as<double>();
   const int64_t* dvn = vnext.as<int64_t>();
 
+  trace("checks + K0 vertices");
   // ---- K2 edge walk
   DBuf cnt, off;
   RB_CUDA(cnt.alloc((nv + 1) * 8));
@@ -1331,6 +1504,7 @@ static int build_impl(const rb_grid* grid, const rb_polygons* P, const rb_build_
   RB_CUDA(cudaGetLastError());
   A->stats.n_partial_leaves = npart;
 
+  trace("K2 edge walk");
   // ---- K3 crossings -> spans
   RB_CUDA(cudaMemsetAsync(cnt.p, 0, (nv + 1) * 8, s));
   if (nv) k_xing_count<<<nblk(nv), 256, 0, s>>>(dgx, dgy, dvn, nv, cnt.as<int64_t>());
@@ -1381,6 +1555,7 @@ static int build_impl(const rb_grid* grid, const rb_polygons* P, const rb_build_
              skey.as<uint64_t>(), sc1.as<int32_t>(), dsoff, dsoff + 1, al.as<double4>(), abeg.as<int64_t>(),
              aend.as<int64_t>()};
 
+  trace("K3 spans + aligned pieces");
   // ---- K4 hierarchical descent
   std::vector<DBuf> cpl, cll, ccl, ckl;
   std::vector<int64_t> ncl;
@@ -1469,6 +1644,7 @@ static int build_impl(const rb_grid* grid, const rb_polygons* P, const rb_build_
     A->stats.n_uniform_interior = (int64_t)h3[2];
   }
 
+  trace("K4 descent + concat + stats");
   int ist = index_impl(L, total_cells, c_poly.as<int32_t>(), c_level.as<uint8_t>(), c_code.as<uint64_t>(),
                        c_kind.as<uint8_t>(), P->poly_region, opts, s, A);
   if (ist) return ist;
@@ -1512,6 +1688,7 @@ extern "C" int rb_approx_build(const rb_grid* grid, const rb_polygons* polys, co
   A->opts = *opts;
   A->n_regions = polys->n_regions;
   A->n_polygons = polys->n_polygons;
+  A->set_code_format();
   int st;
   {
     AllocScope scope((cudaStream_t)stream);  // stream-ordered scratch from the private pool
@@ -1579,6 +1756,7 @@ extern "C" int rb_index_from_cells(const rb_grid* grid, int64_t n_cells, const i
   A->opts.keep_cells = 0;
   A->n_regions = n_regions;
   A->n_polygons = n_cov;
+  A->set_code_format();
   A->stats.max_level = L;
   A->stats.n_regions = n_regions;
   int st = index_impl(L, n_cells, cov, level, code, kind, cov_region, opts, s, A.get());
@@ -1595,46 +1773,50 @@ __global__ void k_hot_remap(const int32_t* regions, int32_t K, int32_t* remap) {
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < K; k += gridDim.x * blockDim.x) remap[regions[k]] = k + 1;
 }
 // annotate single-owner values (root / nodes) with their region's hot slot
-__global__ void k_hot_values(uint32_t* v, int64_t n, const int32_t* remap) {
+__global__ void k_hot_values(uint32_t* v, int64_t n, const int32_t* remap, uint32_t cm, uint32_t hs) {
   GRID_STRIDE(k, n) {
     const uint32_t x = v[k];
     if (x == 0u || (x & (RB_VALUE_NODE | RB_VALUE_LIST))) continue;
-    const uint32_t code = x & RB_CODE_MASK;
+    const uint32_t code = x & cm;
     const uint32_t r = (code - 1u) >> 1;
-    v[k] = code | ((uint32_t)remap[r] << RB_HOT_SHIFT);
+    v[k] = code | ((uint32_t)remap[r] << hs);
   }
 }
-__device__ __forceinline__ uint32_t hot_value(uint32_t x, const int32_t* remap) {
+__device__ __forceinline__ uint32_t hot_value(uint32_t x, const int32_t* remap, uint32_t cm, uint32_t hs) {
   if (x == 0u || (x & (RB_VALUE_NODE | RB_VALUE_LIST))) return x;
-  const uint32_t code = x & RB_CODE_MASK;
-  return code | ((uint32_t)remap[(code - 1u) >> 1] << RB_HOT_SHIFT);
+  const uint32_t code = x & cm;
+  return code | ((uint32_t)remap[(code - 1u) >> 1] << hs);
 }
 // RB_LAYOUT_PACKED: the three palette entries of every block (escape pointers are left alone)
-__global__ void k_hot_blocks(uint4* blk, int64_t n, const int32_t* remap) {
+__global__ void k_hot_blocks(uint4* blk, int64_t n, const int32_t* remap, uint32_t cm, uint32_t hs) {
   GRID_STRIDE(k, n) {
     uint4 b = blk[k];
-    b.x = hot_value(b.x, remap);
-    b.y = hot_value(b.y, remap);
-    b.z = hot_value(b.z, remap);
+    b.x = hot_value(b.x, remap, cm, hs);
+    b.y = hot_value(b.y, remap, cm, hs);
+    b.z = hot_value(b.z, remap, cm, hs);
     blk[k] = b;
   }
 }
-// RB_LAYOUT_KEYS: annotate the single owner values of the cell records
-__global__ void k_hot_records(uint4* rec, int64_t n, const int32_t* remap) {
+__global__ void k_hot_mid(uint4* mid, int64_t n, const int32_t* remap, uint32_t cm, uint32_t hs) {
   GRID_STRIDE(k, n) {
-    const uint32_t x = rec[k].z;
-    if (x == 0u || (x & (RB_VALUE_NODE | RB_VALUE_LIST))) continue;
-    const uint32_t code = x & RB_CODE_MASK;
-    rec[k].z = code | ((uint32_t)remap[(code - 1u) >> 1] << RB_HOT_SHIFT);
+    uint4 b = mid[2 * k];
+    b.x = hot_value(b.x, remap, cm, hs);
+    b.y = hot_value(b.y, remap, cm, hs);
+    b.z = hot_value(b.z, remap, cm, hs);
+    mid[2 * k] = b;
   }
 }
+// RB_LAYOUT_KEYS: annotate the single owner values of the cell records
+__global__ void k_hot_records(uint4* rec, int64_t n, const int32_t* remap, uint32_t cm, uint32_t hs) {
+  GRID_STRIDE(k, n) rec[k].z = hot_value(rec[k].z, remap, cm, hs);
+}
 // annotate owner-list entries ((region<<1)|boundary); count words are flagged
-__global__ void k_hot_pool(uint32_t* p, int64_t n, const int32_t* remap) {
+__global__ void k_hot_pool(uint32_t* p, int64_t n, const int32_t* remap, uint32_t cm, uint32_t hs) {
   GRID_STRIDE(k, n) {
     const uint32_t x = p[k];
     if (x & RB_POOL_COUNT_FLAG) continue;
-    const uint32_t e = x & RB_CODE_MASK;
-    p[k] = e | ((uint32_t)remap[e >> 1] << RB_HOT_SHIFT);
+    const uint32_t e = x & cm;
+    p[k] = e | ((uint32_t)remap[e >> 1] << hs);
   }
 }
 }  // namespace rb
@@ -1647,8 +1829,8 @@ extern "C" int rb_approx_set_hot(rb_approx* a, const int32_t* regions, int32_t n
   using namespace rb;
   if (!a) return fail(RB_CONFIG_ERROR, "null approximation");
   if (a->n_hot) return fail(RB_CONFIG_ERROR, "hot regions already set");
-  if (n_hot < 0 || n_hot > RB_MAX_HOT) return fail(RB_CAPACITY_ERROR, "at most 4095 hot regions");
-  if ((int64_t)a->n_regions >= ((int64_t)1 << 17) - 1) return fail(RB_CAPACITY_ERROR, "hot slots need < 2^17 regions");
+  if (n_hot < 0 || n_hot > a->max_hot)
+    return fail(RB_CAPACITY_ERROR, "at most " + std::to_string(a->max_hot) + " hot regions for this region count");
   if (n_hot == 0) return RB_OK;
   cudaStream_t s = (cudaStream_t)stream;
   AllocScope scope(s);
@@ -1668,18 +1850,23 @@ extern "C" int rb_approx_set_hot(rb_approx* a, const int32_t* regions, int32_t n
   RB_CUDA(remap.alloc((size_t)a->n_regions * 4));
   RB_CUDA(cudaMemsetAsync(remap.p, 0, (size_t)a->n_regions * 4, s));
   k_hot_remap<<<nblk(n_hot), 256, 0, s>>>(a->hot_region.as<int32_t>(), n_hot, remap.as<int32_t>());
-  k_hot_values<<<nblk(a->root_entries), 256, 0, s>>>(a->root.as<uint32_t>(), a->root_entries, remap.as<int32_t>());
+  k_hot_values<<<nblk(a->root_entries), 256, 0, s>>>(a->root.as<uint32_t>(), a->root_entries, remap.as<int32_t>(), a->code_mask, a->hot_shift);
   for (size_t i = 0; i < a->node_bufs.size(); ++i) {
     const int64_t n = (int64_t)(a->node_bufs[i].bytes / 4);
-    k_hot_values<<<nblk(n), 256, 0, s>>>(a->node_bufs[i].as<uint32_t>(), n, remap.as<int32_t>());
+    k_hot_values<<<nblk(n), 256, 0, s>>>(a->node_bufs[i].as<uint32_t>(), n, remap.as<int32_t>(), a->code_mask, a->hot_shift);
   }
-  if (a->n_pblk) k_hot_blocks<<<nblk(a->n_pblk), 256, 0, s>>>(a->pblk.as<uint4>(), a->n_pblk, remap.as<int32_t>());
+  if (a->n_pmid)  // palette halves of the mid sectors (escape pointers and codes are left alone)
+    k_hot_mid<<<nblk(a->n_pmid), 256, 0, s>>>(a->pmid.as<uint4>(), a->n_pmid, remap.as<int32_t>(), a->code_mask, a->hot_shift);
+  if (a->n_pwmid)
+    k_hot_values<<<nblk(a->n_pwmid * 64), 256, 0, s>>>(a->pwmid.as<uint32_t>(), a->n_pwmid * 64, remap.as<int32_t>(),
+                                                        a->code_mask, a->hot_shift);
+  if (a->n_pblk) k_hot_blocks<<<nblk(a->n_pblk), 256, 0, s>>>(a->pblk.as<uint4>(), a->n_pblk, remap.as<int32_t>(), a->code_mask, a->hot_shift);
   if (a->n_pwide)
-    k_hot_values<<<nblk(a->n_pwide * 16), 256, 0, s>>>(a->pwide.as<uint32_t>(), a->n_pwide * 16, remap.as<int32_t>());
-  if (a->pool_len) k_hot_pool<<<nblk(a->pool_len), 256, 0, s>>>(a->pool.as<uint32_t>(), a->pool_len, remap.as<int32_t>());
+    k_hot_values<<<nblk(a->n_pwide * 16), 256, 0, s>>>(a->pwide.as<uint32_t>(), a->n_pwide * 16, remap.as<int32_t>(), a->code_mask, a->hot_shift);
+  if (a->pool_len) k_hot_pool<<<nblk(a->pool_len), 256, 0, s>>>(a->pool.as<uint32_t>(), a->pool_len, remap.as<int32_t>(), a->code_mask, a->hot_shift);
   RB_CUDA(cudaGetLastError());
   if (a->keys.p && a->nkeys)
-    k_hot_records<<<nblk(a->nkeys), 256, 0, s>>>(a->keys.as<uint4>(), a->nkeys, remap.as<int32_t>());
+    k_hot_records<<<nblk(a->nkeys), 256, 0, s>>>(a->keys.as<uint4>(), a->nkeys, remap.as<int32_t>(), a->code_mask, a->hot_shift);
   if (a->S >= 0 && a->keys.p)  // annotated values exceed u16: the summary refers them to the index
     k_key_summary<<<nblk((int64_t)1 << (2 * a->S)), 256, 0, s>>>(a->keys.as<uint4>(), a->nkeys, a->grid.max_level,
                                                                  a->S, a->summary.as<uint16_t>());

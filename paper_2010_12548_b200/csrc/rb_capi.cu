@@ -94,6 +94,8 @@ extern "C" int rb_level_for_bound(double extent, double epsilon, int32_t* level_
 extern "C" int rb_approx_stats(const rb_approx* a, rb_stats* out) {
   if (!a || !out) return fail(RB_CONFIG_ERROR, "null argument");
   *out = a->stats;
+  out->max_hot = a->max_hot;
+  out->n_hot = a->n_hot;
   return RB_OK;
 }
 
@@ -129,7 +131,7 @@ extern "C" int rb_owner_pool(const rb_approx* a, uint32_t* dst, int64_t* n) {
     // public form: count words and (region<<1)|boundary entries, no internal annotations
     std::vector<uint32_t> h(a->pool_len);
     RB_CUDA(cudaMemcpy(h.data(), a->pool.p, a->pool_len * 4, cudaMemcpyDeviceToHost));
-    for (auto& x : h) x = (x & RB_POOL_COUNT_FLAG) ? (x & ~RB_POOL_COUNT_FLAG) : (x & RB_CODE_MASK);
+    for (auto& x : h) x = (x & RB_POOL_COUNT_FLAG) ? (x & ~RB_POOL_COUNT_FLAG) : (x & a->code_mask);
     RB_CUDA(cudaMemcpy(dst, h.data(), a->pool_len * 4, cudaMemcpyDefault));
   }
   return RB_OK;

@@ -27,6 +27,7 @@
 #define RB_CODE_MASK 0x3ffffu
 #define RB_POOL_COUNT_FLAG 0x80000000u
 #define RB_MAX_HOT 4095
+#define RB_MAX_HOT_CAP 16383  // hot slots with narrower owner codes (fewer regions), rb_approx::set_code_format
 // single owner codes ((region << 1) | boundary) + 1 must fit RB_CODE_MASK
 #define RB_MAX_REGIONS (1 << 17)
 
@@ -253,6 +254,15 @@ struct IndexView {
   const uint4* pblk;
   const uint32_t* pwide;
   int pd;
+  // pd >= 6: root slot RB_VALUE_NODE | n -> mid sector n = pmid[2n], pmid[2n + 1] over the root cell's 8x8 mid
+  // cells (2^(pd-3) leaves a side): palette {p0, p1, p2} and 2-bit codes (3 = mixed); escape mids (more than
+  // three owner values: p0 = RB_VALUE_NODE | e) are pwmid[64e + s] (RB_VALUE_NODE = mixed).  The 4x4-leaf
+  // blocks of mixed mid cell s are pblk[(64n + s) * 4^(pd-5) + j], laid out as in the two-level form
+  const uint4* pmid;
+  const uint32_t* pwmid;
+  // owner-value format: code = value & code_mask; hot slot + 1 = value >> hot_shift (bits up to 29)
+  uint32_t code_mask;
+  uint32_t hot_shift;
 };
 
 // RB_LAYOUT_PACKED helpers: the block of leaf (ix, iy) in the root cell whose first block is b, and the
@@ -265,6 +275,22 @@ __device__ __forceinline__ uint32_t packed_slot(uint32_t ix, uint32_t iy) { retu
 __device__ __forceinline__ uint32_t packed_pick(const uint4& k, uint32_t s) {
   const uint32_t i = (k.w >> (2u * s)) & 3u;
   return i == 0u ? k.x : (i == 1u ? k.y : k.z);
+}
+// three-level form: the mid cell of leaf (ix, iy) (its low pd bits) and its leaf block
+__device__ __forceinline__ uint32_t mid_slot(uint32_t ix, uint32_t iy, int pd) {
+  return (((iy >> (pd - 3)) & 7u) << 3) | ((ix >> (pd - 3)) & 7u);
+}
+__device__ __forceinline__ size_t mid_block(uint32_t n, uint32_t ms, uint32_t ix, uint32_t iy, int pd) {
+  const int bw = pd - 5;
+  const uint32_t bm = (1u << bw) - 1u;
+  return ((((size_t)n << 6) | ms) << (2 * bw)) + ((((iy >> 2) & bm) << bw) | ((ix >> 2) & bm));
+}
+// mid sector decode: palette value, or RB_VALUE_NODE for a mixed mid cell (escape mids resolved by one load)
+__device__ __forceinline__ uint32_t mid_pick(const uint4& pal, uint32_t code_word, uint32_t ms, const uint32_t* pwmid) {
+  const uint32_t c = (code_word >> (2u * (ms & 15u))) & 3u;
+  uint32_t v = c == 0u ? pal.x : (c == 1u ? pal.y : (c == 2u ? pal.z : RB_VALUE_NODE));
+  if (c == 0u && (pal.x & RB_VALUE_NODE)) v = __ldg(pwmid + (((size_t)(pal.x & RB_VALUE_PAYLOAD)) << 6) + ms);
+  return v;
 }
 
 __device__ __forceinline__ uint64_t spread_bits(uint32_t v) {
@@ -320,6 +346,20 @@ __device__ __forceinline__ uint32_t index_lookup(const IndexView& v, uint32_t ix
   if (v.krec) return keys_lookup(v, ix, iy);
   int s = v.L - v.T0;
   uint32_t val = __ldg(&v.root[((size_t)(iy >> s) << v.T0) | (ix >> s)]);
+  if (v.pmid) {
+    if (val & RB_VALUE_NODE) {
+      const uint32_t n = val & RB_VALUE_PAYLOAD, ms = mid_slot(ix, iy, v.pd);
+      const uint4 pal = __ldg(v.pmid + 2 * (size_t)n);
+      const uint32_t cw = __ldg(((const uint32_t*)(v.pmid + 2 * (size_t)n + 1)) + (ms >> 4));
+      val = mid_pick(pal, cw, ms, v.pwmid);
+      if (val & RB_VALUE_NODE) {
+        const uint32_t sl = packed_slot(ix, iy);
+        val = packed_pick(__ldg(v.pblk + mid_block(n, ms, ix, iy, v.pd)), sl);
+        if (val & RB_VALUE_NODE) val = __ldg(v.pwide + (((size_t)(val & RB_VALUE_PAYLOAD)) << 4) + sl);
+      }
+    }
+    return val;
+  }
   if (v.pblk) {
     if (val & RB_VALUE_NODE) {
       const uint32_t sl = packed_slot(ix, iy);
@@ -359,10 +399,24 @@ struct rb_approx {
   int64_t nkeys = 0;
   int kshift = 0;
   rb::DBuf pblk, pwide;  // RB_LAYOUT_PACKED: palette blocks (uint4) and escape blocks (16 x u32)
-  int64_t n_pblk = 0, n_pwide = 0;
+  rb::DBuf pmid, pwmid;  // RB_LAYOUT_PACKED, pd >= 6: mid sectors (2 x uint4) and escape mids (64 x u32)
+  int64_t n_pblk = 0, n_pwide = 0, n_pmid = 0, n_pwmid = 0;
   int pd = 0;
   rb::DBuf hot_region;  // int32 [n_hot]: hot slot -> region
   int32_t n_hot = 0;
+  // Owner codes ((region << 1) | boundary) + 1 take code_bits = bit length of 2 * n_regions (<= 18); the hot
+  // slot annotation (slot + 1) sits above them, up to bit 29: 2^(30 - code_bits) - 1 slots (4095 .. 16383)
+  uint32_t code_mask = RB_CODE_MASK, hot_shift = RB_HOT_SHIFT;
+  int32_t max_hot = RB_MAX_HOT;
+  void set_code_format() {
+    uint32_t cb = 1;
+    while (cb < 18 && ((uint64_t)2 * (uint64_t)n_regions) >> cb) ++cb;
+    if (cb < 16) cb = 16;
+    code_mask = (1u << cb) - 1u;
+    hot_shift = cb;
+    const int64_t mh = ((int64_t)1 << (30 - cb)) - 1;
+    max_hot = (int32_t)(mh < RB_MAX_HOT_CAP ? mh : RB_MAX_HOT_CAP);
+  }
   // optional exports
   rb::DBuf cell_poly, cell_level, cell_code, cell_kind;
   int64_t n_cells = 0;
@@ -371,7 +425,7 @@ struct rb_approx {
   rb_stats stats{};
   // buffers kept past the build no longer belong to the build stream
   void detach_all() {
-    for (rb::DBuf* b : {&root, &pool, &summary, &keys, &ktab, &pblk, &pwide, &hot_region, &cell_poly, &cell_level,
+    for (rb::DBuf* b : {&root, &pool, &summary, &keys, &ktab, &pblk, &pwide, &pmid, &pwmid, &hot_region, &cell_poly, &cell_level,
                         &cell_code, &cell_kind, &part_poly, &part_code, &part_kept})
       b->detach();
     for (auto& b : node_bufs) b.detach();
@@ -394,7 +448,11 @@ struct rb_approx {
     v.kshift = kshift;
     v.pblk = pblk.as<uint4>();
     v.pwide = pwide.as<uint32_t>();
+    v.pmid = pmid.as<uint4>();
+    v.pwmid = pwmid.as<uint32_t>();
     v.pd = pd;
+    v.code_mask = code_mask;
+    v.hot_shift = hot_shift;
     return v;
   }
 };

@@ -13,7 +13,9 @@
 // kernel reduces the rows in CTA order -- deterministic, no global atomics.
 // Region sets too large for shared memory accumulate straight into global
 // memory with native REDG.ADD.64 / REDG.ADD.F64.
+#include <algorithm>
 #include <atomic>
+#include <cstdio>
 #include <cstdlib>
 #include <climits>
 #include <mutex>
@@ -119,7 +121,7 @@ __device__ __forceinline__ void point(const PassArgs& a, Hist<SMEM, ATTR>& h, do
   if (val == 0) return;
   double w = (double)wf;
   if (!(val & RB_VALUE_LIST)) {
-    uint32_t s = (val & RB_CODE_MASK) - 1u;
+    uint32_t s = (val & a.V.code_mask) - 1u;
     uint32_t q = s & ~1u;  // 2 * region
     h.add(q, w);
     if (s & 1u) h.add(q + 1, w);
@@ -127,7 +129,7 @@ __device__ __forceinline__ void point(const PassArgs& a, Hist<SMEM, ATTR>& h, do
     const uint32_t* L = a.V.pool + (val & RB_VALUE_PAYLOAD);
     uint32_t k = __ldg(L) & ~RB_POOL_COUNT_FLAG;
     for (uint32_t e = 1; e <= k; ++e) {
-      uint32_t ent = __ldg(L + e) & RB_CODE_MASK;
+      uint32_t ent = __ldg(L + e) & a.V.code_mask;
       uint32_t q = ent & ~1u;
       h.add(q, w);
       if (ent & 1u) h.add(q + 1, w);
@@ -296,10 +298,10 @@ struct IHist {
 
 template <bool ATTR>
 __device__ __noinline__ void add_owners_i(IHist<ATTR> h, const uint32_t* __restrict__ pool, uint32_t v, float w,
-                                          int32_t qv, bool fast) {
+                                          int32_t qv, bool fast, uint32_t cm, uint32_t hs) {
   if (!(v & RB_VALUE_LIST)) {
-    const uint32_t sv = (v & RB_CODE_MASK) - 1u, q = sv & ~1u;
-    h.add(q, v >> RB_HOT_SHIFT, w, qv, fast);
+    const uint32_t sv = (v & cm) - 1u, q = sv & ~1u;
+    h.add(q, v >> hs, w, qv, fast);
     if (sv & 1u) h.add(q + 1, 0u, w, qv, fast);
     return;
   }
@@ -307,9 +309,9 @@ __device__ __noinline__ void add_owners_i(IHist<ATTR> h, const uint32_t* __restr
   const uint32_t kk = __ldg(Lp) & ~RB_POOL_COUNT_FLAG;
   for (uint32_t e = 1; e <= kk; ++e) {
     const uint32_t x = __ldg(Lp + e);
-    const uint32_t ent = x & RB_CODE_MASK;
+    const uint32_t ent = x & cm;
     const uint32_t q = ent & ~1u;
-    h.add(q, x >> RB_HOT_SHIFT, w, qv, fast);
+    h.add(q, x >> hs, w, qv, fast);
     if (ent & 1u) h.add(q + 1, 0u, w, qv, fast);
   }
 }
@@ -363,9 +365,9 @@ __device__ __noinline__ uint64_t quantize_exact(const void* xy, int64_t pidx, in
 // Rare path 2: owner lists and boundary owners (multi-owner cells).
 template <bool ATTR>
 __device__ __noinline__ void add_owners(SHist<ATTR> h, const uint32_t* __restrict__ pool, uint32_t v, float w,
-                                        int32_t qv, bool fast) {
+                                        int32_t qv, bool fast, uint32_t cm) {
   if (!(v & RB_VALUE_LIST)) {
-    const uint32_t sv = (v & RB_CODE_MASK) - 1u, q = sv & ~1u;
+    const uint32_t sv = (v & cm) - 1u, q = sv & ~1u;
     h.add(q, w, qv, fast);
     if (sv & 1u) h.add(q + 1, w, qv, fast);
     return;
@@ -373,7 +375,7 @@ __device__ __noinline__ void add_owners(SHist<ATTR> h, const uint32_t* __restric
   const uint32_t* Lp = pool + (v & RB_VALUE_PAYLOAD);
   const uint32_t kk = __ldg(Lp) & ~RB_POOL_COUNT_FLAG;
   for (uint32_t e = 1; e <= kk; ++e) {
-    const uint32_t ent = __ldg(Lp + e) & RB_CODE_MASK;
+    const uint32_t ent = __ldg(Lp + e) & cm;
     const uint32_t q = ent & ~1u;
     h.add(q, w, qv, fast);
     if (ent & 1u) h.add(q + 1, w, qv, fast);
@@ -548,11 +550,11 @@ __global__ void __launch_bounds__(256, RB_MINB) k_point_pass(PassArgs a) {
           fast = (aw < wmax) & ((aw >= wmin) | (aw == 0.f));
           qv = __float2int_rn(w[i] * sc);
         }
-        const uint32_t sv = (v & RB_CODE_MASK) - 1u;
+        const uint32_t sv = (v & a.V.code_mask) - 1u;
         if (v != 0u && !(v & RB_VALUE_LIST) && (sv & 1u) == 0u) {
           if (fast) h.add_fast(sv, qv); else h.add_slow(sv, w[i]);
         } else if (v != 0u) {
-          add_owners<ATTR>(h, c.pool, v, w[i], qv, fast);
+          add_owners<ATTR>(h, c.pool, v, w[i], qv, fast, a.V.code_mask);
         }
       }
     }
@@ -575,8 +577,8 @@ __global__ void __launch_bounds__(256, RB_MINB) k_point_pass(PassArgs a) {
       const uint32_t v = index_lookup(a.V, qx, qy);
       if (v == 0) continue;
       const float ww = ATTR ? a.attr[i] : 0.f;
-      if (!(v & RB_VALUE_LIST) && !(((v & RB_CODE_MASK) - 1u) & 1u)) h.add_slow((v & RB_CODE_MASK) - 1u, ww);
-      else add_owners<ATTR>(h, c.pool, v, ww, 0, false);
+      if (!(v & RB_VALUE_LIST) && !(((v & a.V.code_mask) - 1u) & 1u)) h.add_slow((v & a.V.code_mask) - 1u, ww);
+      else add_owners<ATTR>(h, c.pool, v, ww, 0, false, a.V.code_mask);
     }
   }
   __syncthreads();
@@ -643,6 +645,23 @@ __device__ __forceinline__ uint32_t mbar_try(uint64_t* bar, uint32_t parity) {
 __device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t parity) {
   while (!__all_sync(0xffffffffu, mbar_try(bar, parity))) {
   }
+}
+// the same on a precomputed shared-memory address (keeps the address computation out of the loop)
+__device__ __forceinline__ uint32_t mbar_try_a(uint32_t addr, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 100000;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity)
+      : "memory");
+  return ok;
+}
+__device__ __forceinline__ void mbar_wait_warp_a(uint32_t addr, uint32_t parity) {
+  while (!__all_sync(0xffffffffu, mbar_try_a(addr, parity))) {
+  }
+}
+__device__ __forceinline__ void mbar_arrive_a(uint32_t addr) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(addr) : "memory");
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
   asm volatile(
@@ -839,9 +858,9 @@ __global__ void __launch_bounds__(RB_CONS + 32, RB_MINB_TMA) k_point_pass_tma(Pa
       const uint32_t v = val[j];
       const bool fast = !ATTR || ((fastm >> j) & 1u);
       // single interior owner: code = v & CODE_MASK (= 2*region + 1), hot slot in bits 18..29
-      const uint32_t sv = (v & RB_CODE_MASK) - 1u;
+      const uint32_t sv = (v & a.V.code_mask) - 1u;
       const bool common = (v != 0u) & ((v & RB_VALUE_LIST) == 0u) & ((sv & 1u) == 0u) & fast;
-      if (common) h.add(sv, v >> RB_HOT_SHIFT, w[j], qv[j], true);
+      if (common) h.add(sv, v >> a.V.hot_shift, w[j], qv[j], true);
       rarem |= (!common & (v != 0u)) ? (1u << j) : 0u;
     }
     // E. boundary owners, owner lists, out-of-window attributes
@@ -850,7 +869,7 @@ __global__ void __launch_bounds__(RB_CONS + 32, RB_MINB_TMA) k_point_pass_tma(Pa
       for (int j = 0; j < RB_PPT; ++j) {
         if (rarem & (1u << j)) {
           const bool fast = !ATTR || ((fastm >> j) & 1u);
-          add_owners_i<ATTR>(h, pool, val[j], w[j], qv[j], fast);
+          add_owners_i<ATTR>(h, pool, val[j], w[j], qv[j], fast, a.V.code_mask, a.V.hot_shift);
         }
       }
     }
@@ -872,7 +891,7 @@ __global__ void __launch_bounds__(RB_CONS + 32, RB_MINB_TMA) k_point_pass_tma(Pa
     const uint64_t qq = quantize_exact(a.xy, i, XY, ox, oy, a.side, a.lim, a.first_bad, a.idx_base);
     if (qq != ~0ull) {
       const uint32_t v = index_lookup(a.V, (uint32_t)qq, (uint32_t)(qq >> 32));
-      if (v != 0u) add_owners_i<ATTR>(h, pool, v, ATTR ? a.attr[i] : 0.f, 0, false);
+      if (v != 0u) add_owners_i<ATTR>(h, pool, v, ATTR ? a.attr[i] : 0.f, 0, false, a.V.code_mask, a.V.hot_shift);
     }
   }
   asm volatile("bar.sync 1, %0;" ::"r"(RB_CONS) : "memory");
@@ -942,18 +961,18 @@ __device__ __forceinline__ void reds(uint32_t addr, uint32_t v) {
 // owner entry adds to exactly one bin.
 template <bool ATTR>
 __device__ __forceinline__ void add_owners_w(uint32_t bins, double* slow, const uint32_t* __restrict__ pool, uint32_t v,
-                                          float w, int32_t qv, bool fast) {
+                                          float w, int32_t qv, bool fast, uint32_t cm) {
   uint32_t n = 1, e = v;
   const uint32_t* Lp = nullptr;
   if (v & RB_VALUE_LIST) {
     Lp = pool + (v & RB_VALUE_PAYLOAD);
     n = __ldg(Lp) & ~RB_POOL_COUNT_FLAG;
   } else {
-    e = (v & RB_CODE_MASK) - 1u;  // (region << 1) | boundary
+    e = (v & cm) - 1u;  // (region << 1) | boundary
   }
 #pragma unroll 1
   for (uint32_t i = 0; i < n; ++i) {
-    if (Lp) e = __ldg(Lp + 1 + i) & RB_CODE_MASK;
+    if (Lp) e = __ldg(Lp + 1 + i) & cm;
     const uint32_t ad = bins + e * (ATTR ? 12u : 4u);
     reds(ad, 1u);
     if (ATTR) {
@@ -1108,7 +1127,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, NW <= 8 ? 2 : 1) k_point_pass_ri
       const uint2 it = rq[(qh + lane) & 63];
       const float ww = __uint_as_float(it.y);
       const bool fast = !ATTR || (((it.y & 0x7fffffffu) - wminb) < wspan);
-      add_owners_w<ATTR>(bins, slow, pool, it.x, ww, ATTR ? __float2int_rn(ww * sc) : 0, fast);
+      add_owners_w<ATTR>(bins, slow, pool, it.x, ww, ATTR ? __float2int_rn(ww * sc) : 0, fast, a.V.code_mask);
     }
     __syncwarp();
   };
@@ -1155,7 +1174,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, NW <= 8 ? 2 : 1) k_point_pass_ri
         // (v == 0, no owner, lands on bin -1: the dummy slot before copy 0, or >= 3 pad words of the copy before)
         const bool common = ((v & RB_VALUE_LIST) == 0u) & fast;
         // unconditional REDs (a predicated RED becomes a branch): off-path points hit this lane's dummy bin
-        const uint32_t ad = common ? h3s + (v & RB_CODE_MASK) * BS : dms;
+        const uint32_t ad = common ? h3s + (v & a.V.code_mask) * BS : dms;
         reds(ad, 1u);
         if (ATTR) {
           reds(ad + 4, (uint32_t)qv & 0xffffu);
@@ -1346,7 +1365,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, NW <= 8 ? 2 : 1) k_point_pass_ri
     const uint64_t qq = quantize_exact(a.xy, i, XY, ox, oy, a.side, a.lim, a.first_bad, a.idx_base);
     if (qq != ~0ull) {
       const uint32_t v = index_lookup(a.V, (uint32_t)qq, (uint32_t)(qq >> 32));
-      if (v != 0u) add_owners_w<ATTR>(bins, slow, pool, v, ATTR ? a.attr[i] : 0.f, 0, false);
+      if (v != 0u) add_owners_w<ATTR>(bins, slow, pool, v, ATTR ? a.attr[i] : 0.f, 0, false, a.V.code_mask);
     }
   }
   asm volatile("bar.sync 1, %0;" ::"r"(NW * 32) : "memory");  // consumers only (the producer has left)
@@ -1393,22 +1412,24 @@ __global__ void __launch_bounds__(NW * 32 + 32, NW <= 8 ? 2 : 1) k_point_pass_ri
 // ---------------------------------------------------------------------------
 template <bool ATTR>
 __device__ __forceinline__ void add_owners_g(uint32_t bins, const uint32_t* __restrict__ pool, uint32_t v, float w,
-                                             int32_t qv, bool fast, unsigned long long* gcnt, double* gsum) {
+                                             int32_t qv, bool fast, unsigned long long* gcnt, double* gsum, uint32_t cm,
+                                             uint32_t hs) {
+  const uint32_t hm = ((1u << (30 - hs)) - 1u) << hs;  // hot field
   uint32_t n = 1, x = v;
   const uint32_t* Lp = nullptr;
   if (v & RB_VALUE_LIST) {
     Lp = pool + (v & RB_VALUE_PAYLOAD);
     n = __ldg(Lp) & ~RB_POOL_COUNT_FLAG;
   } else {
-    x = ((v & RB_CODE_MASK) - 1u) | (v & (RB_HOT_BITS << RB_HOT_SHIFT));  // (region << 1) | boundary, hot slot
+    x = ((v & cm) - 1u) | (v & hm);  // (region << 1) | boundary, hot slot
   }
 #pragma unroll 1
   for (uint32_t i = 0; i < n; ++i) {
     if (Lp) {
       const uint32_t y = __ldg(Lp + 1 + i);
-      x = (y & RB_CODE_MASK) | (y & (RB_HOT_BITS << RB_HOT_SHIFT));
+      x = (y & cm) | (y & hm);
     }
-    const uint32_t e = x & RB_CODE_MASK, q = e & ~1u, slot = (x >> RB_HOT_SHIFT) & RB_HOT_BITS;
+    const uint32_t e = x & cm, q = e & ~1u, slot = x >> hs;
     if (slot && !(e & 1u) && fast) {  // privatised alpha slot
       const uint32_t ad = bins + (slot - 1u) * (ATTR ? 12u : 4u);
       reds(ad, 1u);
@@ -1440,7 +1461,7 @@ __device__ __forceinline__ void redg_sum(double* p, double w, bool pred) {
 // 2 = no palette-block loads (every point of a mixed root cell counts as hot slot 0), 4 = no root loads
 template <int XY, bool ATTR, int NW, int PPT, int NST, int LAY = 0, int ABL = 0>
 __global__ void __launch_bounds__(NW * 32 + 32, 1) k_point_pass_deep(PassArgs a) {
-  constexpr bool KEYS = LAY == 1, PK = LAY == 2;
+  constexpr bool KEYS = LAY == 1, PK = LAY == 2, PK3 = LAY == 3;
   constexpr int PB = XY == 0 ? 16 : 8;
   constexpr int WT = PPT * 32;
   constexpr int TP = NW * WT;
@@ -1556,6 +1577,8 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) k_point_pass_deep(PassArgs a)
   const uint32_t bins = smem_u32(h3) + (uint32_t)((lane & (C - 1)) * P) * 4u;
   const uint32_t h3s = bins - BS;  // hot field (slot + 1) -> slot bin at h3s + field * BS
   const uint32_t dms = smem_u32(dummy) + lane * BS;
+  const uint32_t cmask = a.V.code_mask, hsh = a.V.hot_shift;
+  const uint32_t full_a = smem_u32(full), empty_a = smem_u32(empty);  // mbarrier addresses, hoisted
   unsigned long long* gcnt = a.gcnt;
   double* gsum = a.gsum;
   int qh = 0, qn = 0;
@@ -1564,13 +1587,18 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) k_point_pass_deep(PassArgs a)
       const uint2 it = rq[(qh + lane) & 63];
       const float ww = __uint_as_float(it.y);
       const bool fast = !ATTR || (((it.y & 0x7fffffffu) - wminb) < wspan);
-      add_owners_g<ATTR>(bins, pool, it.x, ww, ATTR ? __float2int_rn(ww * sc) : 0, fast, gcnt, gsum);
+      add_owners_g<ATTR>(bins, pool, it.x, ww, ATTR ? __float2int_rn(ww * sc) : 0, fast, gcnt, gsum, a.V.code_mask,
+                          a.V.hot_shift);
     }
     __syncwarp();
   };
   uint32_t rv[PPT], c1[PPT], c2[PPT], nv1[PPT], nv2[PPT];
   uint32_t hv[PPT], zh[PPT];  // KEYS: radix bucket end (~0u: answered) and the leaf code's high word (c1: low word)
-  uint4 pb[PPT];              // PK: palette blocks loaded in B1 (c2: the leaf's slot in its block)
+  uint4 pb[PPT];              // PK: palette blocks loaded in B1 (c2: the leaf's slot in its block); PK3: in B2
+  uint4 pm[PPT];              // PK3: mid sector palettes loaded in B1 (nv1: the code word, hv: the root value)
+  uint32_t c3[PPT];           // PK3: leaf slot in its block
+  const uint4* __restrict__ pmid = a.V.pmid;
+  const uint32_t* __restrict__ pwmid = a.V.pwmid;
   const uint4* __restrict__ pblk = a.V.pblk;
   const uint32_t* __restrict__ pwide = a.V.pwide;
   const int pd = a.V.pd;
@@ -1580,6 +1608,8 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) k_point_pass_deep(PassArgs a)
     rv[j] = c1[j] = c2[j] = nv1[j] = nv2[j] = 0u;
     w1[j] = w2[j] = w3[j] = 0.f;
     pb[j] = make_uint4(0u, 0u, 0u, 0u);
+    pm[j] = make_uint4(0u, 0u, 0u, 0u);
+    c3[j] = hv[j] = 0u;
   }
   int st = 0;
   uint32_t ph = 0;
@@ -1590,6 +1620,19 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) k_point_pass_deep(PassArgs a)
   for (int64_t k = 0; k < K + CD; ++k) {
     // ------------------------------------------------------------ C(k-CD)
     if (k >= CD) {
+      if constexpr (PK3) {  // leaf palette select (blocks loaded in B2); escape blocks take one more load
+        bool esc = false;
+#pragma unroll
+        for (int j = 0; j < PPT; ++j) {
+          nv2[j] = packed_pick(pb[j], c3[j]);
+          esc |= (int32_t)nv2[j] < 0;
+        }
+        if (__any_sync(0xffffffffu, esc)) {
+#pragma unroll
+          for (int j = 0; j < PPT; ++j)
+            nv2[j] = ldg_pred(pwide + ((size_t)(nv2[j] & RB_VALUE_PAYLOAD) << 4) + c3[j], (int32_t)nv2[j] < 0, nv2[j]);
+        }
+      }
       if constexpr (PK) {  // palette select; escape blocks (> 3 owner values) load their leaf's value
         bool esc = false;
 #pragma unroll
@@ -1614,7 +1657,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) k_point_pass_deep(PassArgs a)
           qv = __float2int_rn(w3[j] * sc);
           fast = ((__float_as_uint(w3[j]) & 0x7fffffffu) - wminb) < wspan;
         }
-        const uint32_t hot = (v >> RB_HOT_SHIFT) & RB_HOT_BITS;
+        const uint32_t hot = (v & ~(RB_VALUE_NODE | RB_VALUE_LIST)) >> hsh;
         // interior single owner with an in-window attribute: a hot region's privatised slot, else
         // predicated global REDs on its alpha bin; everything else takes the rare queue
         const bool single = ((v & (RB_VALUE_LIST | 1u)) == 1u) & fast;
@@ -1626,7 +1669,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) k_point_pass_deep(PassArgs a)
           reds(ad + 8, (uint32_t)(qv >> 16));
         }
         const bool cold = single & (hot == 0u);
-        const uint32_t q = (v & RB_CODE_MASK) - 1u;
+        const uint32_t q = (v & cmask) - 1u;
         if constexpr (!(ABL & 1)) {
           redg_count(gcnt + q, cold);
           if (ATTR) redg_sum(gsum + q, (double)w3[j], cold);
@@ -1669,6 +1712,36 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) k_point_pass_deep(PassArgs a)
     // ------------------------------------------------------------ B2(k-2): node levels 1..
     if constexpr (PK) {  // (no second node stage: C selects from the block)
     } else
+    if constexpr (PK3) {  // mid sector decode, then the 4x4-leaf block of a mixed mid cell
+      if (k >= 2 && k <= K + 1) {
+        bool esc = false;
+        uint32_t mv[PPT], ms[PPT];
+#pragma unroll
+        for (int j = 0; j < PPT; ++j) {
+          w3[j] = w2[j];
+          const uint32_t lx = c2[j] & 0xffffu, ly = c2[j] >> 16;
+          ms[j] = mid_slot(lx, ly, pd);
+          c3[j] = packed_slot(lx, ly);
+          const uint32_t c = (nv1[j] >> (2u * (ms[j] & 15u))) & 3u;
+          const uint32_t v = c == 0u ? pm[j].x : (c == 1u ? pm[j].y : (c == 2u ? pm[j].z : RB_VALUE_NODE));
+          mv[j] = (int32_t)hv[j] < 0 ? v : hv[j];
+          esc |= ((int32_t)hv[j] < 0) & (c == 0u) & ((int32_t)pm[j].x < 0);
+        }
+        if (__any_sync(0xffffffffu, esc)) {  // escape mid sector: the slot's value from the wide mid
+#pragma unroll
+          for (int j = 0; j < PPT; ++j) {
+            const bool e = ((int32_t)hv[j] < 0) & ((int32_t)pm[j].x < 0);
+            mv[j] = ldg_pred(pwmid + ((size_t)(pm[j].x & RB_VALUE_PAYLOAD) << 6) + ms[j], e, mv[j]);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < PPT; ++j) {
+          const bool leaf = ((int32_t)hv[j] < 0) & ((int32_t)mv[j] < 0);
+          const uint32_t lx = c2[j] & 0xffffu, ly = c2[j] >> 16;
+          pb[j] = ldg4_pred(pblk + mid_block(hv[j] & RB_VALUE_PAYLOAD, ms[j], lx, ly, pd), leaf, mv[j]);
+        }
+      }
+    } else
     if constexpr (KEYS) {
       if (k >= 2 && k <= K + 1) {
 #pragma unroll
@@ -1707,6 +1780,21 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) k_point_pass_deep(PassArgs a)
       }
     }
     // ------------------------------------------------------------ B1(k-1): node level 0
+    if constexpr (PK3) {  // the mid sector's palette and code word of each point in a mixed root cell
+      if (k >= 1 && k <= K) {
+#pragma unroll
+        for (int j = 0; j < PPT; ++j) {
+          w2[j] = w1[j];
+          c2[j] = c1[j];
+          hv[j] = rv[j];
+          const bool nd = (int32_t)rv[j] < 0;
+          const size_t n = rv[j] & RB_VALUE_PAYLOAD;
+          const uint32_t ms = mid_slot(c1[j] & 0xffffu, c1[j] >> 16, pd);
+          pm[j] = ldg4_pred(pmid + 2 * n, nd, rv[j]);
+          nv1[j] = ldg_pred(((const uint32_t*)(pmid + 2 * n + 1)) + (ms >> 4), nd, 0u);
+        }
+      }
+    } else
     if constexpr (PK) {  // the 16-byte palette block of each point in a mixed root cell
       if (k >= 1 && k <= K) {
 #pragma unroll
@@ -1715,7 +1803,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) k_point_pass_deep(PassArgs a)
           const uint32_t lx = c1[j] & 0xffffu, ly = c1[j] >> 16;
           c2[j] = packed_slot(lx, ly);
           if constexpr (ABL & 2)
-            pb[j] = make_uint4((int32_t)rv[j] < 0 ? (1u << RB_HOT_SHIFT) | 1u : rv[j], 0u, 0u, 0u);
+            pb[j] = make_uint4((int32_t)rv[j] < 0 ? (1u << hsh) | 1u : rv[j], 0u, 0u, 0u);
           else
             pb[j] = ldg4_pred(pblk + packed_block(rv[j] & RB_VALUE_PAYLOAD, lx, ly, pd), (int32_t)rv[j] < 0, rv[j]);
         }
@@ -1752,7 +1840,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) k_point_pass_deep(PassArgs a)
     // ------------------------------------------------------------ A(k)
     if (k < K) {
       const int64_t t = blockIdx.x + k * G;
-      mbar_wait_warp(&full[st], ph);
+      mbar_wait_warp_a(full_a + 8u * st, ph);
       const unsigned char* tile = smem + (size_t)st * STAGE;
       double x[PPT], y[PPT];
 #pragma unroll
@@ -1769,7 +1857,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) k_point_pass_deep(PassArgs a)
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[st]);
+      if (lane == 0) mbar_arrive_a(empty_a + 8u * st);
       if (++st == NST) { st = 0; ph ^= 1u; }
       uint32_t bx[PPT], by[PPT];
       bool anybad = false;
@@ -1827,7 +1915,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) k_point_pass_deep(PassArgs a)
       for (int j = 0; j < PPT; ++j) {
         const uint32_t* rp = root + (((by[j] >> s0) << T0) | (bx[j] >> s0));
         if constexpr (ABL & 4)
-          rv[j] = (1u << RB_HOT_SHIFT) | 1u + (rp == nullptr);
+          rv[j] = (1u << hsh) | 1u + (rp == nullptr);
         else
           rv[j] = ldg_pred(rp, sv[j] == 0xffffu, sv[j]);
         c1[j] = (bx[j] & m0) | ((by[j] & m0) << 16);
@@ -1842,7 +1930,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) k_point_pass_deep(PassArgs a)
     const uint64_t qq = quantize_exact(a.xy, i, XY, ox, oy, a.side, a.lim, a.first_bad, a.idx_base);
     if (qq != ~0ull) {
       const uint32_t v = index_lookup(a.V, (uint32_t)qq, (uint32_t)(qq >> 32));
-      if (v != 0u) add_owners_g<ATTR>(bins, pool, v, ATTR ? a.attr[i] : 0.f, 0, false, gcnt, gsum);
+      if (v != 0u) add_owners_g<ATTR>(bins, pool, v, ATTR ? a.attr[i] : 0.f, 0, false, gcnt, gsum, a.V.code_mask, a.V.hot_shift);
     }
   }
   asm volatile("bar.sync 1, %0;" ::"r"(NW * 32) : "memory");
@@ -2059,13 +2147,45 @@ static cudaError_t warp_run(const PassArgs& a, size_t smem, cudaStream_t s, int*
 
 template <int XY, bool ATTR, int LAY = 0>
 static cudaError_t warp_dispatch(int ci, const PassArgs& a, size_t smem, cudaStream_t s, int* blocks, bool launch) {
-  if constexpr (LAY != 0) return warp_run<XY, ATTR, 16, 4, 3, LAY>(a, smem, s, blocks, launch);  // the default shape only
+  if constexpr (LAY == 3) return cudaErrorNotSupported;  // the three-level packed index: deep kernel only
+  else if constexpr (LAY != 0) return warp_run<XY, ATTR, 16, 4, 3, LAY>(a, smem, s, blocks, launch);  // default shape only
   switch (ci) {
     case 0: return warp_run<XY, ATTR, 16, 4, 3>(a, smem, s, blocks, launch);
     case 1: return warp_run<XY, ATTR, 16, 4, 4>(a, smem, s, blocks, launch);
     case 2: return warp_run<XY, ATTR, 16, 4, 2>(a, smem, s, blocks, launch);
     default: return warp_run<XY, ATTR, 15, 4, 2>(a, smem, s, blocks, launch);
   }
+}
+
+// Experiments (RB_PERSIST_MB = persisting L2 carve-out, RB_PERSIST_HIT = hit ratio): an L2 access policy
+// window over the root table, so that the index's first level is not evicted by the point stream.
+static bool persist_window(const PassArgs& a, cudaLaunchAttribute* at) {
+  static int mb = -1;
+  static float hr = 1.f;
+  static size_t maxwin = 0;
+  if (mb < 0) {
+    const char* e = getenv("RB_PERSIST_MB");
+    mb = e ? atoi(e) : 0;
+    if (const char* h = getenv("RB_PERSIST_HIT")) hr = (float)atof(h);
+    if (mb > 0) {
+      int dev = 0, mx = 0, mw = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&mx, cudaDevAttrMaxPersistingL2CacheSize, dev);
+      cudaDeviceGetAttribute(&mw, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+      size_t want = std::min<size_t>((size_t)mb << 20, (size_t)mx);
+      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+      maxwin = (size_t)mw;
+      fprintf(stderr, "rb: persisting L2 %zu of max %d bytes, window max %d bytes\n", want, mx, mw);
+    }
+  }
+  if (mb <= 0) return false;
+  at->id = cudaLaunchAttributeAccessPolicyWindow;
+  at->val.accessPolicyWindow.base_ptr = (void*)a.V.root;
+  at->val.accessPolicyWindow.num_bytes = std::min<size_t>(((size_t)4) << (2 * a.V.T0), maxwin);
+  at->val.accessPolicyWindow.hitRatio = hr;
+  at->val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  at->val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  return true;
 }
 
 template <int XY, bool ATTR, int NW, int PPT, int NST, int LAY = 0, int ABL = 0>
@@ -2084,8 +2204,14 @@ static cudaError_t deep_run(const PassArgs& a, size_t smem, cudaStream_t s, int*
   }
   *blocks = cached_blocks;
   if (!launch || cached_blocks <= 0) return cudaSuccess;
-  kern<<<cached_blocks, NW * 32 + 32, smem, s>>>(a);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cached_blocks);
+  cfg.blockDim = dim3(NW * 32 + 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  if (persist_window(a, &at[0])) { cfg.attrs = at; cfg.numAttrs = 1; }
+  return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
 // C4 (200M points, 4095 hot slots): 3 stages + 1 hot-slot copy 1.64 ms; 2 stages 1.67; 4 stages 1.73;
@@ -2103,6 +2229,18 @@ static cudaError_t deep_dispatch(int ci, const PassArgs& a, size_t smem, cudaStr
       case 7: return deep_run<XY, ATTR, 16, 4, 3, LAY, 7>(a, smem, s, blocks, launch);
       case 6: return deep_run<XY, ATTR, 16, 4, 3, LAY, 6>(a, smem, s, blocks, launch);
       default: break;
+    }
+  }
+  if constexpr (LAY == 3) {  // shapes (RB_PK3_CFG): 0 = 15 warps x 4 points (128 registers), 1 = 16 x 4 (96),
+                             // 2 = 16 x 3, 3 = 16 x 2, 4 = 15 x 3
+    static int cfg = -1;
+    if (cfg < 0) { const char* e = getenv("RB_PK3_CFG"); cfg = e ? atoi(e) : 0; }
+    switch (cfg) {
+      case 1: return deep_run<XY, ATTR, 16, 4, 3, LAY>(a, smem, s, blocks, launch);
+      case 2: return deep_run<XY, ATTR, 16, 3, 3, LAY>(a, smem, s, blocks, launch);
+      case 3: return deep_run<XY, ATTR, 16, 2, 3, LAY>(a, smem, s, blocks, launch);
+      case 4: return deep_run<XY, ATTR, 15, 3, 3, LAY>(a, smem, s, blocks, launch);
+      default: return deep_run<XY, ATTR, 15, 4, 3, LAY>(a, smem, s, blocks, launch);
     }
   }
   if constexpr (LAY != 0) return deep_run<XY, ATTR, 16, 4, 3, LAY>(a, smem, s, blocks, launch);  // default shape only
@@ -2127,13 +2265,13 @@ static cudaError_t deep_dispatch(int ci, const PassArgs& a, size_t smem, cudaStr
 #define RB_DISPATCH_LAY(FN, ...)                                                                      \
   (dtype == RB_XY_F64                                                                                 \
        ? (attr ? (lay == 1 ? FN<0, true, 1>(__VA_ARGS__) : lay == 2 ? FN<0, true, 2>(__VA_ARGS__)     \
-                                                                    : FN<0, true, 0>(__VA_ARGS__))    \
+                  : lay == 3 ? FN<0, true, 3>(__VA_ARGS__) : FN<0, true, 0>(__VA_ARGS__))                  \
                : (lay == 1 ? FN<0, false, 1>(__VA_ARGS__) : lay == 2 ? FN<0, false, 2>(__VA_ARGS__)   \
-                                                                     : FN<0, false, 0>(__VA_ARGS__))) \
+                  : lay == 3 ? FN<0, false, 3>(__VA_ARGS__) : FN<0, false, 0>(__VA_ARGS__)))               \
        : (attr ? (lay == 1 ? FN<1, true, 1>(__VA_ARGS__) : lay == 2 ? FN<1, true, 2>(__VA_ARGS__)     \
-                                                                    : FN<1, true, 0>(__VA_ARGS__))    \
+                  : lay == 3 ? FN<1, true, 3>(__VA_ARGS__) : FN<1, true, 0>(__VA_ARGS__))                  \
                : (lay == 1 ? FN<1, false, 1>(__VA_ARGS__) : lay == 2 ? FN<1, false, 2>(__VA_ARGS__)   \
-                                                                     : FN<1, false, 0>(__VA_ARGS__))))
+                  : lay == 3 ? FN<1, false, 3>(__VA_ARGS__) : FN<1, false, 0>(__VA_ARGS__))))
 
 // flags: bit0 = zero the outputs first, bit1 = reset first_bad first
 int point_pass(const rb_approx* A, const void* xy, int32_t dtype, int64_t n, const float* attr, int64_t* cnt_out,
@@ -2181,7 +2319,7 @@ int point_pass(const rb_approx* A, const void* xy, int32_t dtype, int64_t n, con
   const bool vec = ((uintptr_t)xy % 32 == 0) && (!attr || (uintptr_t)attr % (dtype == RB_XY_F64 ? 8 : 16) == 0);
   const bool keys = A->keys.p != nullptr;  // RB_LAYOUT_KEYS: the ring kernel (KEYS) or the generic kernels
   const bool packed = A->pblk.p != nullptr;  // RB_LAYOUT_PACKED: ring / deep kernels (PK) or the generic kernel
-  const int lay = keys ? 1 : (packed ? 2 : 0);
+  const int lay = keys ? 1 : (packed ? (A->pmid.p ? 3 : 2) : 0);
   const bool use_tma = g_kernel_sel != 0 && aligned && !keys && !packed;
   // histogram placement: every bin in shared memory when it fits next to the ring
   const bool smem_hist = use_tma ? ring + all_bins + summ_bytes <= RB_SMEM_BUDGET
@@ -2218,7 +2356,7 @@ int point_pass(const rb_approx* A, const void* xy, int32_t dtype, int64_t n, con
   size_t smem = 0;
   // per-warp rings: shared-memory histogram, L <= 20 (the 2^20 quantisation window)
   int wci = -1;
-  if (g_kernel_sel != 0 && aligned && smem_hist && L <= 20 && g_kernel_sel != 3) {
+  if (g_kernel_sel != 0 && aligned && smem_hist && L <= 20 && g_kernel_sel != 3 && lay != 3) {
     static int env_ci = -2;
     if (env_ci == -2) {
       const char* e = getenv("RB_WARP_CFG");
@@ -2394,7 +2532,7 @@ __global__ void k_lookup(IndexView V, double ox, double oy, double side, double 
       continue;
     }
     const uint32_t v = index_lookup(V, (uint32_t)fx, (uint32_t)fy);
-    out[i] = (v & RB_VALUE_LIST) ? v : (v & RB_CODE_MASK);  // public encoding (no hot annotation)
+    out[i] = (v & RB_VALUE_LIST) ? v : (v & V.code_mask);  // public encoding (no hot annotation)
   }
 }
 

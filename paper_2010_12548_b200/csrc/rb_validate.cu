@@ -52,11 +52,11 @@ __global__ void k_validate(IndexView V, double ox, double oy, double side, doubl
       const uint32_t* Lp = V.pool + (v & RB_VALUE_PAYLOAD);
       const uint32_t k = Lp[0] & ~RB_POOL_COUNT_FLAG;
       for (uint32_t e = 1; e <= k; ++e) {
-        const int32_t r = (int32_t)((Lp[e] & RB_CODE_MASK) >> 1);
+        const int32_t r = (int32_t)((Lp[e] & V.code_mask) >> 1);
         if (na < RB_VAL_MAXSET) { if (!set_has(aset, na, r)) aset[na++] = r; } else ++ovf;
       }
     } else if (v != 0u) {
-      aset[na++] = (int32_t)(((v & RB_CODE_MASK) - 1u) >> 1);
+      aset[na++] = (int32_t)(((v & V.code_mask) - 1u) >> 1);
     }
     // exact owner regions among the bucket's candidate polygons
     int32_t eset[RB_VAL_MAXSET];

@@ -11,6 +11,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -61,6 +62,7 @@ class ApproxIndex:
         self._h = h
         self._torch = torch
         self._hot = None
+        self._hot_lock = threading.Lock()
 
     # regions beyond what one CTA's shared memory holds are accumulated with
     # global atomics; the most frequent owners are privatised ("hot" slots)
@@ -74,11 +76,15 @@ class ApproxIndex:
                                             N.stream_ptr()), "set_hot")
         self._hot = r.numpy().copy()
 
+    # hot slots the deep point pass keeps in shared memory next to its point ring (12 bytes per slot)
+    DEFAULT_HOT = 4095  # 8191 fit the shared memory too, but ran slower (C4: 1.79 -> 2.60 ms per 200M points)
+
     def auto_hot(self, xy, k: int | None = None, sample: int = 1 << 20) -> np.ndarray:
         """Pick the k most frequent single owners of a strided point sample."""
         torch = self._torch
         if k is None:
-            k = int(os.environ.get("RB_HOT_K", N.MAX_HOT))  # RB_HOT_K: experiments
+            k = int(os.environ.get("RB_HOT_K", self.DEFAULT_HOT))  # RB_HOT_K: experiments
+        k = min(k, int(self.stats()["max_hot"]))
         t, _ = self._xy(xy)
         n = int(t.shape[0])
         if n == 0:
@@ -108,6 +114,7 @@ class ApproxIndex:
         self._h = handle
         self._torch = N.require_cuda()
         self._hot = None
+        self._hot_lock = threading.Lock()
         return self
 
     def __del__(self):
@@ -140,20 +147,36 @@ class ApproxIndex:
         t = t.to("cuda", non_blocking=True).contiguous()
         return t, (N.XY_F64 if t.dtype == torch.float64 else N.XY_F32)
 
+    def _ensure_hot(self, xy) -> None:
+        """Large region sets: privatise the most frequent owners once (first pass), under a lock so that
+        concurrent first passes do not both rewrite the index."""
+        if self._hot is None and self.n_regions > self.HOT_THRESHOLD:
+            with self._hot_lock:
+                if self._hot is None:
+                    self.auto_hot(xy)
+
     def point_pass(self, xy, attr=None, out: PassResult | None = None, accumulate: bool = False,
                    stream=None) -> PassResult:
-        """Stream-ordered alpha/beta COUNT + SUM over device points (no host sync)."""
+        """Stream-ordered alpha/beta COUNT + SUM over device points (no host sync).  A float64
+        attribute is summed as its float32 high part plus the float32 residual (two passes)."""
         torch = self._torch
+        if accumulate and out is None:
+            raise E.ConfigError("accumulate=True adds into existing outputs: pass out=")
         t, dt = self._xy(xy)
         n = int(t.shape[0])
-        if self._hot is None and self.n_regions > self.HOT_THRESHOLD:
-            self.auto_hot(t)
-        a = None
+        self._ensure_hot(t)
+        a = lo = None
         if attr is not None:
             a = attr if isinstance(attr, torch.Tensor) else torch.as_tensor(np.asarray(attr))
-            a = a.to("cuda", dtype=torch.float32, non_blocking=True).contiguous()
+            a = a.to("cuda", non_blocking=True)
             if a.shape[0] != n:
                 raise E.ShapeError("attribute length differs from the point count")
+            if a.dtype == torch.float64:
+                hi = a.to(torch.float32)
+                lo = (a - hi.to(torch.float64)).to(torch.float32).contiguous()
+                a = hi.contiguous()
+            else:
+                a = a.to(torch.float32).contiguous()
         if out is None:
             out = PassResult(torch.empty((self.n_regions, 2), dtype=torch.int64, device="cuda"),
                              torch.empty((self.n_regions, 2), dtype=torch.float64, device="cuda"),
@@ -161,6 +184,12 @@ class ApproxIndex:
         N.check(self._lib.rb_point_pass(self._h, t.data_ptr(), dt, n, a.data_ptr() if a is not None else None,
                                         out.cnt.data_ptr(), out.sum.data_ptr(), out.first_bad.data_ptr(),
                                         1 if accumulate else 0, N.stream_ptr(stream)), "join")
+        if lo is not None:  # the residual part's sums (its counts repeat the first pass)
+            part = PassResult(torch.empty_like(out.cnt), torch.empty_like(out.sum), torch.empty_like(out.first_bad))
+            N.check(self._lib.rb_point_pass(self._h, t.data_ptr(), dt, n, lo.data_ptr(), part.cnt.data_ptr(),
+                                            part.sum.data_ptr(), part.first_bad.data_ptr(), 0, N.stream_ptr(stream)),
+                    "join")
+            out.sum.add_(part.sum)
         return out
 
     def join_host(self, xy: np.ndarray, attr: np.ndarray | None = None):
@@ -168,7 +197,16 @@ class ApproxIndex:
         xy = np.ascontiguousarray(xy) if isinstance(xy, np.ndarray) else xy
         if self._hot is None and self.n_regions > self.HOT_THRESHOLD:
             step = max(1, int(xy.shape[0]) // (1 << 20))
-            self.auto_hot(xy[::step])
+            self._ensure_hot(xy[::step])
+        if attr is not None:  # float64: float32 high part + float32 residual, two joins
+            dt64 = attr.dtype == np.float64 if isinstance(attr, np.ndarray) else attr.dtype == self._torch.float64
+            if dt64:
+                a64 = np.asarray(attr.numpy() if hasattr(attr, "numpy") else attr, np.float64)
+                hi = a64.astype(np.float32)
+                lo = (a64 - hi.astype(np.float64)).astype(np.float32)
+                cnt, sm = self.join_host(xy, hi)
+                _, sm_lo = self.join_host(xy, lo)
+                return cnt, sm + sm_lo
         if isinstance(xy, np.ndarray):
             dt = N.XY_F64 if xy.dtype == np.float64 else N.XY_F32
             if xy.dtype not in (np.float64, np.float32):

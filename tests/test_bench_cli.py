@@ -13,7 +13,17 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def _json_lines(out: str):
-    return [json.loads(x) for x in out.splitlines() if x.startswith("{")]
+    """Every JSON object in the output (ranks may write concurrently)."""
+    dec = json.JSONDecoder()
+    objs, i = [], out.find("{")
+    while i >= 0:
+        try:
+            o, end = dec.raw_decode(out, i)
+            objs.append(o)
+            i = out.find("{", end)
+        except json.JSONDecodeError:
+            i = out.find("{", i + 1)
+    return objs
 
 
 @pytest.mark.timeout(300)

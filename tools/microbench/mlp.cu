@@ -1,0 +1,114 @@
+// Random-lookup throughput vs memory-level parallelism (design aid for the point
+// pass's index lookups).  Every thread issues PPT random 4-byte lookups per
+// iteration into a table of `mb` MB and consumes them one iteration later:
+//   mode 0: ld.global.nc.u32            (L1-allocating; in-flight misses hold L1 lines)
+//   mode 1: ld.global.nc.L1::no_allocate.u32
+//   mode 2: cp.async.cg.shared.global 16 B (L2 only) into a per-thread shared-memory slot,
+//           cp.async.commit_group / wait_group 1
+// The kernel also reserves `pad` KB of shared memory to emulate the point pass's ring.
+// Output: one JSON line per (table size, mode, PPT, warps, pad).
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+
+__device__ __forceinline__ uint32_t xs(uint32_t& s) { s ^= s << 13; s ^= s >> 17; s ^= s << 5; return s; }
+
+template <int MODE, int PPT>
+__global__ void k(const uint32_t* __restrict__ tab, uint32_t mask16, int iters, uint32_t* out) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  uint4* slot = (uint4*)sm + (size_t)threadIdx.x * PPT * 2;  // 2 stages x PPT x 16 B per thread
+  uint32_t s = 0x9e3779b9u * (blockIdx.x * blockDim.x + threadIdx.x + 1);
+  uint32_t acc = 0;
+  uint32_t v[PPT];
+#pragma unroll
+  for (int j = 0; j < PPT; ++j) v[j] = 0;
+  for (int it = 0; it < iters; ++it) {
+    const int st = it & 1;
+    if (MODE == 2) {
+#pragma unroll
+      for (int j = 0; j < PPT; ++j) {
+        const uint32_t q = xs(s) & mask16;  // 16-byte granule
+        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&slot[st * PPT + j]);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(tab + (size_t)q * 4) : "memory");
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+#pragma unroll
+      for (int j = 0; j < PPT; ++j) acc += slot[(st ^ 1) * PPT + j].x;
+    } else {
+#pragma unroll
+      for (int j = 0; j < PPT; ++j) acc += v[j];
+#pragma unroll
+      for (int j = 0; j < PPT; ++j) {
+        const uint32_t q = xs(s) & mask16;
+        const uint32_t* p = tab + (size_t)q * 4;
+        if (MODE == 0) asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(v[j]) : "l"(p));
+        else asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v[j]) : "l"(p));
+      }
+    }
+  }
+  if (MODE == 2) asm volatile("cp.async.wait_group 0;" ::: "memory");
+  if (acc == 0x12345678u) out[0] = acc;
+}
+
+template <int MODE, int PPT>
+static void run(const uint32_t* tab, size_t mb, int warps, int pad_kb, int sms, int clk, uint32_t* out) {
+  const int threads = warps * 32;
+  const size_t smem = (size_t)threads * PPT * 32 + (size_t)pad_kb * 1024;
+  if (smem > 227 * 1024) return;
+  auto kern = k<MODE, PPT>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  const uint32_t mask16 = (uint32_t)((mb << 20) / 16 - 1);
+  const int iters = 400;
+  kern<<<sms, threads, smem>>>(tab, mask16, iters, out);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a);
+  kern<<<sms, threads, smem>>>(tab, mask16, iters, out);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  const double n = (double)sms * threads * iters * PPT;
+  printf("{\"table_mb\":%zu,\"mode\":%d,\"ppt\":%d,\"warps\":%d,\"smem_kb\":%zu,\"err\":\"%s\",\"Glookups_s\":%.1f,"
+         "\"lookups_per_sm_clk\":%.3f}\n",
+         mb, MODE, PPT, warps, smem / 1024, cudaGetErrorString(cudaGetLastError()), n / ms / 1e6,
+         n / (ms * 1e-3) / sms / (clk * 1e3));
+  fflush(stdout);
+}
+
+int main() {
+  int sms, clk;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  if (const char* g = getenv("MLP_SMS")) sms = atoi(g);  // CTAs (one per SM): per-SM vs chip-wide limits
+  cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+  const size_t maxmb = 4096;
+  uint32_t* tab;
+  uint32_t* out;
+  cudaMalloc(&tab, maxmb << 20);
+  cudaMemset(tab, 1, maxmb << 20);
+  cudaMalloc(&out, 16);
+  const char* sweep = getenv("MLP_SWEEP");
+  if (sweep && sweep[0] == '2') {  // in-flight depth: warps x lookups per thread, L2-resident table
+    for (size_t mb : {32ul, 256ul})
+      for (int warps : {8, 16, 32})
+        for (int pad : {0, 128}) {
+          run<0, 4>(tab, mb, warps, pad, sms, clk, out);
+          run<0, 8>(tab, mb, warps, pad, sms, clk, out);
+          run<0, 16>(tab, mb, warps, pad, sms, clk, out);
+          run<1, 8>(tab, mb, warps, pad, sms, clk, out);
+        }
+    return 0;
+  }
+  for (size_t mb : {32ul, 4096ul})
+    for (int pad : {0, 96, 160})
+      for (int warps : {16}) {
+        run<0, 4>(tab, mb, warps, pad, sms, clk, out);
+        run<0, 8>(tab, mb, warps, pad, sms, clk, out);
+        run<1, 4>(tab, mb, warps, pad, sms, clk, out);
+        run<2, 4>(tab, mb, warps, pad, sms, clk, out);
+        run<2, 8>(tab, mb, warps, pad, sms, clk, out);
+      }
+  return 0;
+}
