@@ -7,7 +7,7 @@
 
 Default workload: C4, the largest single-GPU config of BASELINE.json (1B f32
 points, 40,000 polygons, eps = 1 m, hierarchical raster, COUNT + SUM) on the
-epsilon-matched grid (leaf side eps/sqrt(2)) with the packed cell index.
+epsilon-matched grid (leaf side eps/sqrt(2)) with the radix-table cell index.
 
 One step = one point pass over this rank's batch of synthetic points (inputs
 resident in HBM, approximation prebuilt and replicated on every GPU), plus
@@ -247,7 +247,7 @@ def run_ours(a):
     C = CONFIGS[a.config]
     n = a.points or C["points"]
     w = workload(a.config, n, rank, a.grid)
-    layout = a.layout or ("dense" if a.config == "c1" else ("packed" if a.config == "c4" else "trie"))
+    layout = a.layout or ("dense" if a.config == "c1" else "trie")
     agg = C["agg"]
     q = AggregationQuery(agg, w.epsilon, RasterMode.CONSERVATIVE)
     prep = PreparedJoin(w.regions, q, w.grid, layout=layout, root_level=a.root_level)

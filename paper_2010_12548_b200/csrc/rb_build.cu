@@ -693,11 +693,45 @@ __device__ inline int fill_level(const IndexBuild& B, int l) {
   for (int i = 0; i < B.nlev; ++i) { T += B.ks[i]; if (l <= T) return T; }
   return T;
 }
+// rows of the positions whose square spans more than 2^RB_FILL_WARP_D x 2^RB_FILL_WARP_D slots (smaller squares
+// take k_fill_small, single slots k_fill_single)
+#define RB_FILL_WARP_D 5
 __global__ void k_fill_rows(IndexBuild B, const uint8_t* plevel, int64_t npos, int lo_excl, int hi_incl,
                             int64_t* rows) {
   GRID_STRIDE(P, npos) {
     int l = plevel[P];
-    rows[P] = (l > lo_excl && l <= hi_incl) ? (1ll << (fill_level(B, l) - l)) : 0;
+    const int d = fill_level(B, l) - l;
+    rows[P] = (l > lo_excl && l <= hi_incl && d > RB_FILL_WARP_D) ? (1ll << d) : 0;
+  }
+}
+// positions whose square is 2^d x 2^d slots with 1 <= d <= RB_FILL_WARP_D: one warp per position, row by row
+__global__ void k_fill_small(IndexBuild B, const uint64_t* pstart, const uint8_t* plevel, const uint32_t* pval,
+                             int64_t npos, int lo_excl, int hi_incl) {
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t P = warp; P < npos; P += nw) {
+    const int l = plevel[P];
+    if (!(l > lo_excl && l <= hi_incl)) continue;
+    const int T = fill_level(B, l), d = T - l;
+    if (d < 1 || d > RB_FILL_WARP_D) continue;
+    const uint64_t code = pstart[P] >> (2 * (B.L - l));
+    const uint64_t cx = (uint64_t)compact1by1(code) << d, cy = (uint64_t)compact1by1(code >> 1) << d;
+    const uint32_t w = 1u << d, v = pval[P];
+    for (uint32_t r = 0; r < w; ++r) {
+      uint32_t* base = slot_ptr(B, cx, cy + r, T);
+      for (uint32_t t = lane; t < w; t += 32) base[t] = v;
+    }
+  }
+}
+// positions at a structure level (most of them: boundary leaves): one thread writes the one slot
+__global__ void k_fill_single(IndexBuild B, const uint64_t* pstart, const uint8_t* plevel, const uint32_t* pval,
+                              int64_t npos, int lo_excl, int hi_incl) {
+  GRID_STRIDE(P, npos) {
+    const int l = plevel[P];
+    if (!(l > lo_excl && l <= hi_incl) || fill_level(B, l) != l) continue;
+    const uint64_t code = pstart[P] >> (2 * (B.L - l));
+    *slot_ptr(B, compact1by1(code), compact1by1(code >> 1), l) = pval[P];
   }
 }
 // one warp per row: fill 2^(T-l) slots of row `r` of position P's square
@@ -1284,7 +1318,13 @@ static int index_impl(int L, int64_t total_cells, const int32_t* cp_in, const ui
     RB_CUDA(rows.alloc((npos + 1) * 8));
     RB_CUDA(roff.alloc((npos + 1) * 8));
     RB_CUDA(cudaMemsetAsync(rows.p, 0, (npos + 1) * 8, s));
-    if (npos) k_fill_rows<<<nblk(npos), 256, 0, s>>>(B, plevel.as<uint8_t>(), npos, lo_excl, hi_incl, rows.as<int64_t>());
+    if (npos) {
+      k_fill_rows<<<nblk(npos), 256, 0, s>>>(B, plevel.as<uint8_t>(), npos, lo_excl, hi_incl, rows.as<int64_t>());
+      k_fill_single<<<nblk(npos), 256, 0, s>>>(B, pstart.as<uint64_t>(), plevel.as<uint8_t>(), pval.as<uint32_t>(),
+                                               npos, lo_excl, hi_incl);
+      k_fill_small<<<nblk(npos * 32), 256, 0, s>>>(B, pstart.as<uint64_t>(), plevel.as<uint8_t>(), pval.as<uint32_t>(),
+                                                   npos, lo_excl, hi_incl);
+    }
     RB_CUDA(excl_scan_i64(rows.as<int64_t>(), roff.as<int64_t>(), npos + 1, s));
     int64_t nrows = d2h(roff.as<int64_t>() + npos, s);
     if (nrows) k_fill<<<nblk(nrows * 32), 256, 0, s>>>(B, pstart.as<uint64_t>(), plevel.as<uint8_t>(),

@@ -40,7 +40,8 @@ cudaMemPool_t mem_pool() {
     } else {
       size_t fr = 0, tot = 0;
       cudaMemGetInfo(&fr, &tot);
-      uint64_t thr = tot / 4;  // cache up to a quarter of the device between builds / passes
+      uint64_t thr = tot / 2;  // cache up to half the device between builds / passes (a C4 build peaks near 50 GB;
+                               // trimming below that made every rebuild remap its scratch: 0.5 -> 1.4 s)
       cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &thr);
     }
     pools[dev & 63] = p;

@@ -240,3 +240,41 @@ def test_shard_ranges_partition():
             rs = [shard_range(n, r, world) for r in range(world)]
             assert rs[0][0] == 0 and rs[-1][1] == n
             assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
+
+
+def test_region_sets_beyond_the_owner_code_field_are_rejected():
+    """Owner values carry ((region << 1) | boundary) + 1 in 18 bits: a region set of
+    2^17 or more is a CapacityError before any device work."""
+    from paper_2010_12548_b200 import _native as N
+
+    lib = N.load()
+    g = N.Grid(0.0, 0.0, 1.0, 8)
+    for n_regions, want in ((1 << 17, N.RB_CAPACITY_ERROR if hasattr(N, "RB_CAPACITY_ERROR") else -3), (0, -3)):
+        polys = N.Polygons(None, None, 0, None, 0, None, 0, None, n_regions)
+        opts = N.BuildOpts(0, N.LAYOUT_TRIE, 8, -1, 0)
+        h = ctypes.c_void_p()
+        st = lib.rb_approx_build(ctypes.byref(g), ctypes.byref(polys), ctypes.byref(opts), None, ctypes.byref(h))
+        assert st == want
+        assert "n_regions" in lib.rb_last_error().decode()
+
+
+def test_packed_layout_is_a_known_layout():
+    from paper_2010_12548_b200 import _native as N
+    from paper_2010_12548_b200.engine import LAYOUTS
+
+    assert LAYOUTS == {"dense": 0, "trie": 1, "keys": 2, "packed": 3}
+    hdr = open(os.path.join(ROOT, "include", "rasterbound_b200.h")).read()
+    assert "#define RB_LAYOUT_PACKED 3" in hdr
+    assert N.LAYOUT_PACKED == 3
+
+
+def test_eps_grid_leaf_side_is_eps_over_sqrt2():
+    """grid.eps_grid: side exactly eps/sqrt(2) and level_for_bound returns its level."""
+    from paper_2010_12548_b200.grid import eps_grid, level_for_bound
+
+    for eps, span in ((1.0, 100_000.0), (4.9, 40_000.0), (1e-3, 1.0), (0.5, 40_000.0)):
+        g = eps_grid(0.0, 0.0, span, span, eps)
+        assert math.ldexp(g.extent, -g.max_level) == eps / math.sqrt(2.0)
+        assert g.extent >= 1.02 * span and g.extent / 2 < 1.02 * span
+        assert level_for_bound(g, eps) == g.max_level
+    assert eps_grid(0.0, 0.0, 100_000.0, 100_000.0, 1.0).max_level == 18

@@ -1,4 +1,5 @@
-timeout 1500 python -m pytest tests/test_gpu_scale.py -q -x 2>&1 | tail -5
-for c in 0 1; do for k in 3071 4095 5119; do
-RB_DEEP_CFG=$c RB_HOT_K=$k timeout 300 python tools/profile_pass.py c4 200000000 trie 3 12 2>&1 | grep -E "Gpts" | tail -1 | sed "s/^/TRIE12 cfg=$c K=$k /"
-done; done
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_api.py tests/test_gpu_packed.py -q -x 2>&1 | tail -3
+for spec in "c2 trie -1" "c4 trie -1" "c4 packed -1"; do
+  set -- $spec
+  RB_BUILD_TRACE=1 timeout 600 python tools/build_time.py $1 $2 $3 5 2> gpurun_out/r2_build3_$1_$2.trace | tail -1
+done
