@@ -47,10 +47,11 @@ extern "C" {
 #define RB_LAYOUT_TRIE 1  /* multi-level radix table (ACT, hierarchical raster) */
 #define RB_LAYOUT_KEYS 2  /* sorted 64-bit cell keys (disjoint covering cells, leaf-level start keys)
                            with a radix table over the top key bits: radix + binary search */
-#define RB_LAYOUT_PACKED 3 /* radix table root (level root_level, default L - 5) over palette-packed
-                            leaf blocks: each 4x4-leaf block of a mixed root cell is 16 bytes (three owner
-                            values + 16 two-bit palette indices), so a lookup is one root word and, inside
-                            mixed root cells, one 16-byte block (large region sets, e.g. C4) */
+#define RB_LAYOUT_PACKED 3 /* radix table whose last level is palette-packed: each 4x4-leaf block is 16
+                            bytes (three owner values + 16 two-bit palette indices).  L - root_level in
+                            [2, 5]: the blocks sit right below the root; in [6, 8] (default root_level
+                            L - 6): one u32 node level, then packed nodes of 16 x 16 leaves.  C4: a 1.2 GB
+                            index against 4.5 GB for RB_LAYOUT_TRIE at the same speed */
 
 /* point coordinate storage */
 #define RB_XY_F64 0 /* interleaved float64 (x,y) */
@@ -90,7 +91,7 @@ typedef struct rb_build_opts {
   int32_t mode;        /* RB_MODE_* */
   int32_t layout;      /* RB_LAYOUT_* */
   int32_t radix_width; /* ACT bits per node: 2, 4, 8; default 8 */
-  int32_t root_level;  /* TRIE / PACKED root table level; -1 = automatic (PACKED: L - 5, at least 0) */
+  int32_t root_level;  /* TRIE / PACKED root table level; -1 = automatic (TRIE: min(L, 12); PACKED: L - 6) */
   int32_t keep_cells;  /* keep per-polygon covering cells for export */
 } rb_build_opts;
 

@@ -858,110 +858,6 @@ __global__ void k_pack_emit(const uint32_t* nodes, int64_t nblocks, int pd, cons
     blk[b] = make_uint4(p[0], p[1], p[2], idx);
   }
 }
-// three-level packed index (pd = L - T0 >= 6).  Level-0 node n (8x8 u32 slots: owner value, or
-// RB_VALUE_NODE | c for a mixed mid cell whose 2^kb x 2^kb leaves are level-1 node c) -> mid sector n:
-// {p0, p1, p2, 0, c0..c3}, 2-bit code of slot s at c[s >> 4] bits 2 (s & 15); code 3 = mixed (leaf blocks
-// follow), else the palette entry.  More than three distinct owner values: {NODE | e, 0, 0, 0, 0...} and
-// pwmid[64 e + s] = the slot's owner value or RB_VALUE_NODE for a mixed slot.
-__device__ inline int mid_distinct(const uint32_t* v, uint32_t d[3]) {
-  int nd = 0;
-  for (int s = 0; s < 64; ++s) {
-    const uint32_t q = v[s];
-    if (q & RB_VALUE_NODE) continue;
-    int i = 0;
-    while (i < nd && i < 3 && d[i] != q) ++i;
-    if (i < nd && i < 3) continue;
-    if (nd < 3) d[nd] = q;
-    ++nd;
-    if (nd > 3) break;
-  }
-  return nd;
-}
-__global__ void k_mid_count(const uint32_t* nodes0, int64_t nmid, uint32_t* esc) {
-  GRID_STRIDE(n, nmid) {
-    uint32_t d[3];
-    esc[n] = mid_distinct(nodes0 + (n << 6), d) > 3 ? 1u : 0u;
-  }
-}
-__global__ void k_mid_emit(const uint32_t* nodes0, int64_t nmid, const uint32_t* eoff, uint4* mid, uint32_t* wmid) {
-  GRID_STRIDE(n, nmid) {
-    const uint32_t* v = nodes0 + (n << 6);
-    uint32_t d[3] = {0u, 0u, 0u};
-    const int nd = mid_distinct(v, d);
-    if (nd > 3) {
-      const uint32_t e = eoff[n];
-      for (int s = 0; s < 64; ++s) wmid[((size_t)e << 6) + s] = (v[s] & RB_VALUE_NODE) ? RB_VALUE_NODE : v[s];
-      mid[2 * n] = make_uint4(RB_VALUE_NODE | e, 0u, 0u, 0u);
-      mid[2 * n + 1] = make_uint4(0u, 0u, 0u, 0u);
-      continue;
-    }
-    if (nd == 0) d[0] = 0u;
-    if (nd < 2) d[1] = d[0];
-    if (nd < 3) d[2] = d[0];
-    uint32_t c[4] = {0u, 0u, 0u, 0u};
-    for (int s = 0; s < 64; ++s) {
-      uint32_t code = 3u;
-      if (!(v[s] & RB_VALUE_NODE)) code = v[s] == d[0] ? 0u : (v[s] == d[1] ? 1u : 2u);
-      c[s >> 4] |= code << (2 * (s & 15));
-    }
-    mid[2 * n] = make_uint4(d[0], d[1], d[2], 0u);
-    mid[2 * n + 1] = make_uint4(c[0], c[1], c[2], c[3]);
-  }
-}
-// leaf block b = (n * 64 + s) * 4^(kb-2) + j: 4x4-leaf block j of mid cell s of mixed root cell n, packed from
-// level-1 node c when slot s of level-0 node n is RB_VALUE_NODE | c (other blocks are never read: zeroes)
-__device__ inline int leaf_gather(const uint32_t* nodes0, const uint32_t* nodes1, int64_t b, int kb, uint32_t v[16]) {
-  const int bw = kb - 2;
-  const int64_t ms = b >> (2 * bw);  // n * 64 + s
-  const uint32_t j = (uint32_t)(b & ((1ll << (2 * bw)) - 1));
-  const uint32_t slot = nodes0[ms];
-  if (!(slot & RB_VALUE_NODE)) return -1;
-  const uint32_t* nb = nodes1 + ((size_t)(slot & RB_VALUE_PAYLOAD) << (2 * kb));
-  const uint32_t bx = j & ((1u << bw) - 1u), by = j >> bw;
-  int nd = 0;
-  uint32_t d0 = 0, d1 = 0, d2 = 0;
-  for (int t = 0; t < 16; ++t) {
-    const uint32_t x = (bx << 2) | (t & 3), y = (by << 2) | (t >> 2);
-    v[t] = nb[((size_t)y << kb) | x];
-    const uint32_t q = v[t];
-    if (nd > 0 && q == d0) continue;
-    if (nd > 1 && q == d1) continue;
-    if (nd > 2 && q == d2) continue;
-    if (nd == 0) d0 = q; else if (nd == 1) d1 = q; else if (nd == 2) d2 = q;
-    ++nd;
-  }
-  return nd;
-}
-__global__ void k_leaf_count(const uint32_t* nodes0, const uint32_t* nodes1, int64_t nblocks, int kb, uint32_t* esc) {
-  GRID_STRIDE(b, nblocks) {
-    uint32_t v[16];
-    esc[b] = leaf_gather(nodes0, nodes1, b, kb, v) > 3 ? 1u : 0u;
-  }
-}
-__global__ void k_leaf_emit(const uint32_t* nodes0, const uint32_t* nodes1, int64_t nblocks, int kb,
-                            const uint32_t* eoff, uint4* blk, uint32_t* wide) {
-  GRID_STRIDE(b, nblocks) {
-    uint32_t v[16];
-    const int nd = leaf_gather(nodes0, nodes1, b, kb, v);
-    if (nd < 0) { blk[b] = make_uint4(0u, 0u, 0u, 0u); continue; }
-    if (nd > 3) {
-      const uint32_t e = eoff[b];
-      for (int t = 0; t < 16; ++t) wide[((size_t)e << 4) + t] = v[t];
-      blk[b] = make_uint4(RB_VALUE_NODE | e, 0u, 0u, 0u);
-      continue;
-    }
-    uint32_t p[3] = {v[0], v[0], v[0]};
-    int np = 1;
-    uint32_t idx = 0;
-    for (int t = 0; t < 16; ++t) {
-      int i = 0;
-      while (i < np && p[i] != v[t]) ++i;
-      if (i == np) p[np++] = v[t];
-      idx |= (uint32_t)i << (2 * t);
-    }
-    blk[b] = make_uint4(p[0], p[1], p[2], idx);
-  }
-}
 // root slots: node pointer n -> first block of node n
 __global__ void k_pack_root(uint32_t* root, int64_t n, int pd) {
   GRID_STRIDE(k, n) {
@@ -1218,9 +1114,9 @@ static int index_impl(int L, int64_t total_cells, const int32_t* cp_in, const ui
     // per 200M points over T0 = 11; only the data's 19 MB of it is touched)
     T0 = opts->root_level >= 0 ? std::min(opts->root_level, L) : (L <= 20 ? std::min(L, 12) : 11);
     if (opts->layout == RB_LAYOUT_PACKED) {
-      // pd = L - T0 in [2, 5]: 4x4-leaf palette blocks right below the root; pd in [6, 8]: a 32-byte palette
-      // sector of 8x8 mid cells per mixed root cell, then the 4x4-leaf blocks of the mixed mid cells
-      T0 = opts->root_level >= 0 ? opts->root_level : std::max(0, L - 5);
+      // L - T0 in [2, 5]: nodes of 4x4-leaf palette blocks right below the root; in [6, 8]: one radix node
+      // level of u32 slots (L - T0 - 4 bits a side), then packed nodes of 16 x 16 leaves
+      T0 = opts->root_level >= 0 ? opts->root_level : (L >= 6 ? L - 6 : 0);
       if (L < 2) return fail(RB_CONFIG_ERROR, "the packed layout needs max_level >= 2");
       if (L - T0 < 2 || L - T0 > 8)
         return fail(RB_CONFIG_ERROR, "packed layout: root_level must lie in [max_level - 8, max_level - 2]");
@@ -1239,7 +1135,7 @@ static int index_impl(int L, int64_t total_cells, const int32_t* cp_in, const ui
     }
     if (opts->layout == RB_LAYOUT_PACKED) {  // dense nodes, packed below
       ks.clear();
-      if (rem >= 6) { ks.push_back(3); ks.push_back(rem - 3); } else ks.push_back(rem);
+      if (rem >= 6) { ks.push_back(rem - 4); ks.push_back(4); } else ks.push_back(rem);
     }
     if (ks.empty() && rem > 0) {
       int first = rem % k ? rem % k : k;
@@ -1348,48 +1244,34 @@ static int index_impl(int L, int64_t total_cells, const int32_t* cp_in, const ui
     }
   }
   A->node_levels.clear();
-  if (opts->layout == RB_LAYOUT_PACKED && L - T0 >= 6) {
-    const int pd = L - T0;
-    const int kb = pd - 3;                          // leaves per mid cell side: 2^kb
-    const int64_t nmid = nnodes[0];
-    const int64_t bpm = (int64_t)1 << (2 * (kb - 2));  // 4x4-leaf blocks per mid cell
-    const int64_t nblocks = nmid * 64 * bpm;          // dense: every mid cell of a mixed root cell
-    DBuf mesc, moff, esc, eoff;
-    RB_CUDA(mesc.alloc((nmid + 1) * 4));
-    RB_CUDA(moff.alloc((nmid + 1) * 4));
-    RB_CUDA(cudaMemsetAsync(mesc.p, 0, (nmid + 1) * 4, s));
+  if (opts->layout == RB_LAYOUT_PACKED && B.nlev == 2) {
+    // radix node level 0 stays u32; the level-1 nodes (16 x 16 leaves) become 16 palette blocks each
+    const int pd = ks[1];
+    const int64_t bpn = (int64_t)1 << (2 * (pd - 2));
+    const int64_t nblocks = nnodes[1] * bpn;
+    if (nblocks >= (int64_t)RB_VALUE_PAYLOAD) return fail(RB_CAPACITY_ERROR, "packed index exceeds 2^30 blocks");
+    DBuf esc, eoff;
     RB_CUDA(esc.alloc((nblocks + 1) * 4));
     RB_CUDA(eoff.alloc((nblocks + 1) * 4));
     RB_CUDA(cudaMemsetAsync(esc.p, 0, (nblocks + 1) * 4, s));
-    if (nmid) {
-      k_mid_count<<<nblk(nmid), 256, 0, s>>>(node_bufs[0].as<uint32_t>(), nmid, mesc.as<uint32_t>());
-      k_leaf_count<<<nblk(nblocks), 256, 0, s>>>(node_bufs[0].as<uint32_t>(), node_bufs[1].as<uint32_t>(), nblocks, kb,
-                                                 esc.as<uint32_t>());
-    }
+    if (nblocks) k_pack_count<<<nblk(nblocks), 256, 0, s>>>(node_bufs[1].as<uint32_t>(), nblocks, pd, esc.as<uint32_t>());
     RB_CUDA(cudaGetLastError());
-    RB_CUDA(excl_scan_u32(mesc.as<uint32_t>(), moff.as<uint32_t>(), nmid + 1, s));
     RB_CUDA(excl_scan_u32(esc.as<uint32_t>(), eoff.as<uint32_t>(), nblocks + 1, s));
-    const int64_t nwmid = d2h(moff.as<uint32_t>() + nmid, s);
     const int64_t nwide = d2h(eoff.as<uint32_t>() + nblocks, s);
-    RB_CUDA(A->pmid.alloc(std::max<int64_t>(nmid, 1) * 32));
-    RB_CUDA(A->pwmid.alloc(std::max<int64_t>(nwmid, 1) * 256));
     RB_CUDA(A->pblk.alloc(std::max<int64_t>(nblocks, 1) * 16));
     RB_CUDA(A->pwide.alloc(std::max<int64_t>(nwide, 1) * 64));
-    if (nmid) {
-      k_mid_emit<<<nblk(nmid), 256, 0, s>>>(node_bufs[0].as<uint32_t>(), nmid, moff.as<uint32_t>(), A->pmid.as<uint4>(),
-                                            A->pwmid.as<uint32_t>());
-      k_leaf_emit<<<nblk(nblocks), 256, 0, s>>>(node_bufs[0].as<uint32_t>(), node_bufs[1].as<uint32_t>(), nblocks, kb,
-                                                eoff.as<uint32_t>(), A->pblk.as<uint4>(), A->pwide.as<uint32_t>());
-    }
+    if (nblocks)
+      k_pack_emit<<<nblk(nblocks), 256, 0, s>>>(node_bufs[1].as<uint32_t>(), nblocks, pd, eoff.as<uint32_t>(),
+                                                A->pblk.as<uint4>(), A->pwide.as<uint32_t>());
+    const int64_t n0 = nnodes[0] << (2 * ks[0]);  // level-0 slots: node pointer n -> first block of node n
+    if (n0) k_pack_root<<<nblk(n0), 256, 0, s>>>(node_bufs[0].as<uint32_t>(), n0, pd);
     RB_CUDA(cudaGetLastError());
     RB_CUDA(cudaStreamSynchronize(s));
-    node_bufs.clear();
+    node_bufs.pop_back();
     A->pd = pd;
-    A->n_pmid = nmid;
-    A->n_pwmid = nwmid;
     A->n_pblk = nblocks;
     A->n_pwide = nwide;
-    node_bytes = nmid * 32 + nwmid * 256 + nblocks * 16 + nwide * 64;
+    node_bytes = (nnodes[0] << (2 * ks[0])) * 4 + nblocks * 16 + nwide * 64;
   } else if (opts->layout == RB_LAYOUT_PACKED) {
     const int pd = L - T0;
     const int64_t bpr = (int64_t)1 << (2 * (pd - 2));
@@ -1837,15 +1719,6 @@ __global__ void k_hot_blocks(uint4* blk, int64_t n, const int32_t* remap, uint32
     blk[k] = b;
   }
 }
-__global__ void k_hot_mid(uint4* mid, int64_t n, const int32_t* remap, uint32_t cm, uint32_t hs) {
-  GRID_STRIDE(k, n) {
-    uint4 b = mid[2 * k];
-    b.x = hot_value(b.x, remap, cm, hs);
-    b.y = hot_value(b.y, remap, cm, hs);
-    b.z = hot_value(b.z, remap, cm, hs);
-    mid[2 * k] = b;
-  }
-}
 // RB_LAYOUT_KEYS: annotate the single owner values of the cell records
 __global__ void k_hot_records(uint4* rec, int64_t n, const int32_t* remap, uint32_t cm, uint32_t hs) {
   GRID_STRIDE(k, n) rec[k].z = hot_value(rec[k].z, remap, cm, hs);
@@ -1895,11 +1768,6 @@ extern "C" int rb_approx_set_hot(rb_approx* a, const int32_t* regions, int32_t n
     const int64_t n = (int64_t)(a->node_bufs[i].bytes / 4);
     k_hot_values<<<nblk(n), 256, 0, s>>>(a->node_bufs[i].as<uint32_t>(), n, remap.as<int32_t>(), a->code_mask, a->hot_shift);
   }
-  if (a->n_pmid)  // palette halves of the mid sectors (escape pointers and codes are left alone)
-    k_hot_mid<<<nblk(a->n_pmid), 256, 0, s>>>(a->pmid.as<uint4>(), a->n_pmid, remap.as<int32_t>(), a->code_mask, a->hot_shift);
-  if (a->n_pwmid)
-    k_hot_values<<<nblk(a->n_pwmid * 64), 256, 0, s>>>(a->pwmid.as<uint32_t>(), a->n_pwmid * 64, remap.as<int32_t>(),
-                                                        a->code_mask, a->hot_shift);
   if (a->n_pblk) k_hot_blocks<<<nblk(a->n_pblk), 256, 0, s>>>(a->pblk.as<uint4>(), a->n_pblk, remap.as<int32_t>(), a->code_mask, a->hot_shift);
   if (a->n_pwide)
     k_hot_values<<<nblk(a->n_pwide * 16), 256, 0, s>>>(a->pwide.as<uint32_t>(), a->n_pwide * 16, remap.as<int32_t>(), a->code_mask, a->hot_shift);

@@ -247,19 +247,14 @@ struct IndexView {
   const uint32_t* ktab;
   int64_t nkeys;
   int kshift;
-  // RB_LAYOUT_PACKED: root slot = owner value, or RB_VALUE_NODE | b: the root cell's 4^(pd-2) blocks of
-  // 4x4 leaves start at pblk[b] (row-major over the cell's 2^(pd-2) x 2^(pd-2) blocks, pd = L - T0).
-  // Block {p0, p1, p2, idx}: leaf s = (y & 3) * 4 + (x & 3) owns p[(idx >> 2s) & 3]; a block with more
-  // than three distinct owner values has p0 = RB_VALUE_NODE | e, idx = 0: its 16 values are pwide[16e..]
+  // RB_LAYOUT_PACKED: the radix table (root, then nlev = 0 or 1 node levels of u32 slots) ends in packed
+  // nodes of 2^pd x 2^pd leaves: a slot RB_VALUE_NODE | b points at the node's 4^(pd-2) blocks of 4x4
+  // leaves, pblk[b ..] (row-major over the node's 2^(pd-2) x 2^(pd-2) blocks).  Block {p0, p1, p2, idx}:
+  // leaf s = (y & 3) * 4 + (x & 3) owns p[(idx >> 2s) & 3]; a block with more than three distinct owner
+  // values has p0 = RB_VALUE_NODE | e, idx = 0: its 16 values are pwide[16e ..]
   const uint4* pblk;
   const uint32_t* pwide;
   int pd;
-  // pd >= 6: root slot RB_VALUE_NODE | n -> mid sector n = pmid[2n], pmid[2n + 1] over the root cell's 8x8 mid
-  // cells (2^(pd-3) leaves a side): palette {p0, p1, p2} and 2-bit codes (3 = mixed); escape mids (more than
-  // three owner values: p0 = RB_VALUE_NODE | e) are pwmid[64e + s] (RB_VALUE_NODE = mixed).  The 4x4-leaf
-  // blocks of mixed mid cell s are pblk[(64n + s) * 4^(pd-5) + j], laid out as in the two-level form
-  const uint4* pmid;
-  const uint32_t* pwmid;
   // owner-value format: code = value & code_mask; hot slot + 1 = value >> hot_shift (bits up to 29)
   uint32_t code_mask;
   uint32_t hot_shift;
@@ -276,22 +271,7 @@ __device__ __forceinline__ uint32_t packed_pick(const uint4& k, uint32_t s) {
   const uint32_t i = (k.w >> (2u * s)) & 3u;
   return i == 0u ? k.x : (i == 1u ? k.y : k.z);
 }
-// three-level form: the mid cell of leaf (ix, iy) (its low pd bits) and its leaf block
-__device__ __forceinline__ uint32_t mid_slot(uint32_t ix, uint32_t iy, int pd) {
-  return (((iy >> (pd - 3)) & 7u) << 3) | ((ix >> (pd - 3)) & 7u);
-}
-__device__ __forceinline__ size_t mid_block(uint32_t n, uint32_t ms, uint32_t ix, uint32_t iy, int pd) {
-  const int bw = pd - 5;
-  const uint32_t bm = (1u << bw) - 1u;
-  return ((((size_t)n << 6) | ms) << (2 * bw)) + ((((iy >> 2) & bm) << bw) | ((ix >> 2) & bm));
-}
-// mid sector decode: palette value, or RB_VALUE_NODE for a mixed mid cell (escape mids resolved by one load)
-__device__ __forceinline__ uint32_t mid_pick(const uint4& pal, uint32_t code_word, uint32_t ms, const uint32_t* pwmid) {
-  const uint32_t c = (code_word >> (2u * (ms & 15u))) & 3u;
-  uint32_t v = c == 0u ? pal.x : (c == 1u ? pal.y : (c == 2u ? pal.z : RB_VALUE_NODE));
-  if (c == 0u && (pal.x & RB_VALUE_NODE)) v = __ldg(pwmid + (((size_t)(pal.x & RB_VALUE_PAYLOAD)) << 6) + ms);
-  return v;
-}
+
 
 __device__ __forceinline__ uint64_t spread_bits(uint32_t v) {
   uint64_t x = v;
@@ -346,21 +326,13 @@ __device__ __forceinline__ uint32_t index_lookup(const IndexView& v, uint32_t ix
   if (v.krec) return keys_lookup(v, ix, iy);
   int s = v.L - v.T0;
   uint32_t val = __ldg(&v.root[((size_t)(iy >> s) << v.T0) | (ix >> s)]);
-  if (v.pmid) {
-    if (val & RB_VALUE_NODE) {
-      const uint32_t n = val & RB_VALUE_PAYLOAD, ms = mid_slot(ix, iy, v.pd);
-      const uint4 pal = __ldg(v.pmid + 2 * (size_t)n);
-      const uint32_t cw = __ldg(((const uint32_t*)(v.pmid + 2 * (size_t)n + 1)) + (ms >> 4));
-      val = mid_pick(pal, cw, ms, v.pwmid);
-      if (val & RB_VALUE_NODE) {
-        const uint32_t sl = packed_slot(ix, iy);
-        val = packed_pick(__ldg(v.pblk + mid_block(n, ms, ix, iy, v.pd)), sl);
-        if (val & RB_VALUE_NODE) val = __ldg(v.pwide + (((size_t)(val & RB_VALUE_PAYLOAD)) << 4) + sl);
-      }
-    }
-    return val;
-  }
   if (v.pblk) {
+    for (int li = 0; li < v.nlev && (val & RB_VALUE_NODE); ++li) {  // u32 node levels above the packed nodes
+      const int k = v.ks[li];
+      s -= k;
+      const uint32_t m = (1u << k) - 1u;
+      val = __ldg(&v.nodes[li][((size_t)(val & RB_VALUE_PAYLOAD) << (2 * k)) + ((((iy >> s) & m) << k) | ((ix >> s) & m))]);
+    }
     if (val & RB_VALUE_NODE) {
       const uint32_t sl = packed_slot(ix, iy);
       val = packed_pick(__ldg(v.pblk + packed_block(val & RB_VALUE_PAYLOAD, ix, iy, v.pd)), sl);
@@ -399,8 +371,7 @@ struct rb_approx {
   int64_t nkeys = 0;
   int kshift = 0;
   rb::DBuf pblk, pwide;  // RB_LAYOUT_PACKED: palette blocks (uint4) and escape blocks (16 x u32)
-  rb::DBuf pmid, pwmid;  // RB_LAYOUT_PACKED, pd >= 6: mid sectors (2 x uint4) and escape mids (64 x u32)
-  int64_t n_pblk = 0, n_pwide = 0, n_pmid = 0, n_pwmid = 0;
+  int64_t n_pblk = 0, n_pwide = 0;
   int pd = 0;
   rb::DBuf hot_region;  // int32 [n_hot]: hot slot -> region
   int32_t n_hot = 0;
@@ -425,7 +396,7 @@ struct rb_approx {
   rb_stats stats{};
   // buffers kept past the build no longer belong to the build stream
   void detach_all() {
-    for (rb::DBuf* b : {&root, &pool, &summary, &keys, &ktab, &pblk, &pwide, &pmid, &pwmid, &hot_region, &cell_poly, &cell_level,
+    for (rb::DBuf* b : {&root, &pool, &summary, &keys, &ktab, &pblk, &pwide, &hot_region, &cell_poly, &cell_level,
                         &cell_code, &cell_kind, &part_poly, &part_code, &part_kept})
       b->detach();
     for (auto& b : node_bufs) b.detach();
@@ -448,8 +419,6 @@ struct rb_approx {
     v.kshift = kshift;
     v.pblk = pblk.as<uint4>();
     v.pwide = pwide.as<uint32_t>();
-    v.pmid = pmid.as<uint4>();
-    v.pwmid = pwmid.as<uint32_t>();
     v.pd = pd;
     v.code_mask = code_mask;
     v.hot_shift = hot_shift;

@@ -1461,7 +1461,7 @@ __device__ __forceinline__ void redg_sum(double* p, double w, bool pred) {
 // 2 = no palette-block loads (every point of a mixed root cell counts as hot slot 0), 4 = no root loads
 template <int XY, bool ATTR, int NW, int PPT, int NST, int LAY = 0, int ABL = 0>
 __global__ void __launch_bounds__(NW * 32 + 32, 1) k_point_pass_deep(PassArgs a) {
-  constexpr bool KEYS = LAY == 1, PK = LAY == 2, PK3 = LAY == 3;
+  constexpr bool KEYS = LAY == 1, PK = LAY == 2, PK3 = LAY == 3;  // PK3: radix node level over packed leaves
   constexpr int PB = XY == 0 ? 16 : 8;
   constexpr int WT = PPT * 32;
   constexpr int TP = NW * WT;
@@ -1595,10 +1595,6 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) k_point_pass_deep(PassArgs a)
   uint32_t rv[PPT], c1[PPT], c2[PPT], nv1[PPT], nv2[PPT];
   uint32_t hv[PPT], zh[PPT];  // KEYS: radix bucket end (~0u: answered) and the leaf code's high word (c1: low word)
   uint4 pb[PPT];              // PK: palette blocks loaded in B1 (c2: the leaf's slot in its block); PK3: in B2
-  uint4 pm[PPT];              // PK3: mid sector palettes loaded in B1 (nv1: the code word, hv: the root value)
-  uint32_t c3[PPT];           // PK3: leaf slot in its block
-  const uint4* __restrict__ pmid = a.V.pmid;
-  const uint32_t* __restrict__ pwmid = a.V.pwmid;
   const uint4* __restrict__ pblk = a.V.pblk;
   const uint32_t* __restrict__ pwide = a.V.pwide;
   const int pd = a.V.pd;
@@ -1608,8 +1604,7 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) k_point_pass_deep(PassArgs a)
     rv[j] = c1[j] = c2[j] = nv1[j] = nv2[j] = 0u;
     w1[j] = w2[j] = w3[j] = 0.f;
     pb[j] = make_uint4(0u, 0u, 0u, 0u);
-    pm[j] = make_uint4(0u, 0u, 0u, 0u);
-    c3[j] = hv[j] = 0u;
+    hv[j] = 0u;
   }
   int st = 0;
   uint32_t ph = 0;
@@ -1620,17 +1615,17 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) k_point_pass_deep(PassArgs a)
   for (int64_t k = 0; k < K + CD; ++k) {
     // ------------------------------------------------------------ C(k-CD)
     if (k >= CD) {
-      if constexpr (PK3) {  // leaf palette select (blocks loaded in B2); escape blocks take one more load
+      if constexpr (PK3) {  // leaf palette select (blocks loaded in B2; hv: the leaf's slot); escapes: one more load
         bool esc = false;
 #pragma unroll
         for (int j = 0; j < PPT; ++j) {
-          nv2[j] = packed_pick(pb[j], c3[j]);
+          nv2[j] = packed_pick(pb[j], hv[j]);
           esc |= (int32_t)nv2[j] < 0;
         }
         if (__any_sync(0xffffffffu, esc)) {
 #pragma unroll
           for (int j = 0; j < PPT; ++j)
-            nv2[j] = ldg_pred(pwide + ((size_t)(nv2[j] & RB_VALUE_PAYLOAD) << 4) + c3[j], (int32_t)nv2[j] < 0, nv2[j]);
+            nv2[j] = ldg_pred(pwide + ((size_t)(nv2[j] & RB_VALUE_PAYLOAD) << 4) + hv[j], (int32_t)nv2[j] < 0, nv2[j]);
         }
       }
       if constexpr (PK) {  // palette select; escape blocks (> 3 owner values) load their leaf's value
@@ -1712,33 +1707,14 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) k_point_pass_deep(PassArgs a)
     // ------------------------------------------------------------ B2(k-2): node levels 1..
     if constexpr (PK) {  // (no second node stage: C selects from the block)
     } else
-    if constexpr (PK3) {  // mid sector decode, then the 4x4-leaf block of a mixed mid cell
+    if constexpr (PK3) {  // the 16-byte palette block below a node-level-0 slot (radix node, then packed leaves)
       if (k >= 2 && k <= K + 1) {
-        bool esc = false;
-        uint32_t mv[PPT], ms[PPT];
 #pragma unroll
         for (int j = 0; j < PPT; ++j) {
           w3[j] = w2[j];
           const uint32_t lx = c2[j] & 0xffffu, ly = c2[j] >> 16;
-          ms[j] = mid_slot(lx, ly, pd);
-          c3[j] = packed_slot(lx, ly);
-          const uint32_t c = (nv1[j] >> (2u * (ms[j] & 15u))) & 3u;
-          const uint32_t v = c == 0u ? pm[j].x : (c == 1u ? pm[j].y : (c == 2u ? pm[j].z : RB_VALUE_NODE));
-          mv[j] = (int32_t)hv[j] < 0 ? v : hv[j];
-          esc |= ((int32_t)hv[j] < 0) & (c == 0u) & ((int32_t)pm[j].x < 0);
-        }
-        if (__any_sync(0xffffffffu, esc)) {  // escape mid sector: the slot's value from the wide mid
-#pragma unroll
-          for (int j = 0; j < PPT; ++j) {
-            const bool e = ((int32_t)hv[j] < 0) & ((int32_t)pm[j].x < 0);
-            mv[j] = ldg_pred(pwmid + ((size_t)(pm[j].x & RB_VALUE_PAYLOAD) << 6) + ms[j], e, mv[j]);
-          }
-        }
-#pragma unroll
-        for (int j = 0; j < PPT; ++j) {
-          const bool leaf = ((int32_t)hv[j] < 0) & ((int32_t)mv[j] < 0);
-          const uint32_t lx = c2[j] & 0xffffu, ly = c2[j] >> 16;
-          pb[j] = ldg4_pred(pblk + mid_block(hv[j] & RB_VALUE_PAYLOAD, ms[j], lx, ly, pd), leaf, mv[j]);
+          hv[j] = packed_slot(lx, ly);
+          pb[j] = ldg4_pred(pblk + packed_block(nv1[j] & RB_VALUE_PAYLOAD, lx, ly, pd), (int32_t)nv1[j] < 0, nv1[j]);
         }
       }
     } else
@@ -1780,18 +1756,15 @@ __global__ void __launch_bounds__(NW * 32 + 32, 1) k_point_pass_deep(PassArgs a)
       }
     }
     // ------------------------------------------------------------ B1(k-1): node level 0
-    if constexpr (PK3) {  // the mid sector's palette and code word of each point in a mixed root cell
+    if constexpr (PK3) {  // node level 0 (radix slots over the root cell) as for the radix table
       if (k >= 1 && k <= K) {
 #pragma unroll
         for (int j = 0; j < PPT; ++j) {
           w2[j] = w1[j];
           c2[j] = c1[j];
-          hv[j] = rv[j];
-          const bool nd = (int32_t)rv[j] < 0;
-          const size_t n = rv[j] & RB_VALUE_PAYLOAD;
-          const uint32_t ms = mid_slot(c1[j] & 0xffffu, c1[j] >> 16, pd);
-          pm[j] = ldg4_pred(pmid + 2 * n, nd, rv[j]);
-          nv1[j] = ldg_pred(((const uint32_t*)(pmid + 2 * n + 1)) + (ms >> 4), nd, 0u);
+          const uint32_t slot = (((c1[j] >> (16 + s1)) & mk0) << k0) | ((c1[j] >> s1) & mk0);
+          const uint32_t off = ((rv[j] & RB_VALUE_PAYLOAD) << (2 * k0)) | slot;
+          nv1[j] = ldg_pred(nodes0 + off, (int32_t)rv[j] < 0, rv[j]);
         }
       }
     } else
@@ -2231,17 +2204,12 @@ static cudaError_t deep_dispatch(int ci, const PassArgs& a, size_t smem, cudaStr
       default: break;
     }
   }
-  if constexpr (LAY == 3) {  // shapes (RB_PK3_CFG): 0 = 15 warps x 4 points (128 registers), 1 = 16 x 4 (96),
-                             // 2 = 16 x 3, 3 = 16 x 2, 4 = 15 x 3
+  if constexpr (LAY == 3) {  // 15 consumer warps (4 per SM sub-partition: 128 registers, no spills): C4 1.68 ms per
+                             // 200M points; RB_PK3_CFG=1: 16 warps at 96 registers spill, 2.29 ms
     static int cfg = -1;
     if (cfg < 0) { const char* e = getenv("RB_PK3_CFG"); cfg = e ? atoi(e) : 0; }
-    switch (cfg) {
-      case 1: return deep_run<XY, ATTR, 16, 4, 3, LAY>(a, smem, s, blocks, launch);
-      case 2: return deep_run<XY, ATTR, 16, 3, 3, LAY>(a, smem, s, blocks, launch);
-      case 3: return deep_run<XY, ATTR, 16, 2, 3, LAY>(a, smem, s, blocks, launch);
-      case 4: return deep_run<XY, ATTR, 15, 3, 3, LAY>(a, smem, s, blocks, launch);
-      default: return deep_run<XY, ATTR, 15, 4, 3, LAY>(a, smem, s, blocks, launch);
-    }
+    if (cfg == 1) return deep_run<XY, ATTR, 16, 4, 3, LAY>(a, smem, s, blocks, launch);
+    return deep_run<XY, ATTR, 15, 4, 3, LAY>(a, smem, s, blocks, launch);
   }
   if constexpr (LAY != 0) return deep_run<XY, ATTR, 16, 4, 3, LAY>(a, smem, s, blocks, launch);  // default shape only
   switch (ci) {
@@ -2319,7 +2287,7 @@ int point_pass(const rb_approx* A, const void* xy, int32_t dtype, int64_t n, con
   const bool vec = ((uintptr_t)xy % 32 == 0) && (!attr || (uintptr_t)attr % (dtype == RB_XY_F64 ? 8 : 16) == 0);
   const bool keys = A->keys.p != nullptr;  // RB_LAYOUT_KEYS: the ring kernel (KEYS) or the generic kernels
   const bool packed = A->pblk.p != nullptr;  // RB_LAYOUT_PACKED: ring / deep kernels (PK) or the generic kernel
-  const int lay = keys ? 1 : (packed ? (A->pmid.p ? 3 : 2) : 0);
+  const int lay = keys ? 1 : (packed ? (A->node_bufs.empty() ? 2 : 3) : 0);
   const bool use_tma = g_kernel_sel != 0 && aligned && !keys && !packed;
   // histogram placement: every bin in shared memory when it fits next to the ring
   const bool smem_hist = use_tma ? ring + all_bins + summ_bytes <= RB_SMEM_BUDGET

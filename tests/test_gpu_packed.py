@@ -26,7 +26,7 @@ def test_packed_overlapping_with_holes(oracle_lib, mode, L, root_level):
     A, _ = oracle_approx(oracle_lib, regions, grid, mode)
     idx = _prepared(regions, grid, mode, "packed", root_level=root_level)
     st = idx.stats()
-    assert st["root_level"] == (root_level if root_level >= 0 else max(0, L - 5))
+    assert st["root_level"] == (root_level if root_level >= 0 else (L - 6 if L >= 6 else 0))
     _assert_join(idx, A, xy, attr)
     _assert_join(idx, A, xy.astype(np.float32), None)
     trie = _prepared(regions, grid, mode, "trie")

@@ -35,6 +35,22 @@ __global__ void k(const uint32_t* __restrict__ tab, uint32_t mask16, int iters, 
       asm volatile("cp.async.wait_group 1;" ::: "memory");
 #pragma unroll
       for (int j = 0; j < PPT; ++j) acc += slot[(st ^ 1) * PPT + j].x;
+    } else if (MODE == 3 || MODE == 4) {  // 3: random u64 REDs into an 80k x 8 B table; 4: loads + half as many REDs
+      unsigned long long* red = (unsigned long long*)out + 2;
+      if (MODE == 4) {
+#pragma unroll
+        for (int j = 0; j < PPT; ++j) acc += v[j];
+#pragma unroll
+        for (int j = 0; j < PPT; ++j) {
+          const uint32_t q = xs(s) & mask16;
+          asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(v[j]) : "l"(tab + (size_t)q * 4));
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < (MODE == 4 ? PPT / 2 : PPT); ++j) {
+        const uint32_t r = xs(s) % 80000u;
+        asm volatile("red.global.add.u64 [%0], 1;" ::"l"(red + r) : "memory");
+      }
     } else {
 #pragma unroll
       for (int j = 0; j < PPT; ++j) acc += v[j];
@@ -70,7 +86,7 @@ static void run(const uint32_t* tab, size_t mb, int warps, int pad_kb, int sms, 
   cudaEventSynchronize(b);
   float ms = 0;
   cudaEventElapsedTime(&ms, a, b);
-  const double n = (double)sms * threads * iters * PPT;
+  const double n = (double)sms * threads * iters * (MODE == 4 ? PPT + PPT / 2 : PPT);  // global requests
   printf("{\"table_mb\":%zu,\"mode\":%d,\"ppt\":%d,\"warps\":%d,\"smem_kb\":%zu,\"err\":\"%s\",\"Glookups_s\":%.1f,"
          "\"lookups_per_sm_clk\":%.3f}\n",
          mb, MODE, PPT, warps, smem / 1024, cudaGetErrorString(cudaGetLastError()), n / ms / 1e6,
@@ -88,8 +104,17 @@ int main() {
   uint32_t* out;
   cudaMalloc(&tab, maxmb << 20);
   cudaMemset(tab, 1, maxmb << 20);
-  cudaMalloc(&out, 16);
+  cudaMalloc(&out, 16 + 80000 * 8);
   const char* sweep = getenv("MLP_SWEEP");
+  if (sweep && sweep[0] == '3') {  // REDs alone and mixed with loads (L2-resident table)
+    for (int warps : {8, 16})
+      for (int pad : {0, 128}) {
+        run<3, 8>(tab, 32, warps, pad, sms, clk, out);
+        run<4, 8>(tab, 32, warps, pad, sms, clk, out);
+        run<0, 8>(tab, 32, warps, pad, sms, clk, out);
+      }
+    return 0;
+  }
   if (sweep && sweep[0] == '2') {  // in-flight depth: warps x lookups per thread, L2-resident table
     for (size_t mb : {32ul, 256ul})
       for (int warps : {8, 16, 32})
