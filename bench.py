@@ -316,6 +316,23 @@ def run_ours(a):
             "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
             "kernel": "k_point_pass (ring / deep)", "kernel_ms": round(k_ms, 4),
             "algorithmic_bytes_per_point": C["bpp"], "points_per_launch": n, "index_lookups": lookups}
+    # The second bound: random global requests per point (index sectors + RED sectors,
+    # from the ncu capture) against the SM's measured random-request rates (tools/microbench/mlp)
+    rates_p = os.path.join(ROOT, "profiles", "round2", "request_rates.json")
+    if lookups is not None and os.path.exists(rates_p):
+        with open(rates_p) as f:
+            rates = json.load(f)
+        idx_pp = pj["index_l2_sectors_per_point"]
+        red_pp = pj.get("red_sectors_per_point", 0.0) or 0.0
+        cyc_pp = idx_pp / rates["load_per_sm_clk"] + red_pp / rates["red_per_sm_clk"]
+        clk = (sampler.summary().get("sm_mhz") or 1965) * 1e6
+        sms = torch.cuda.get_device_properties(local).multi_processor_count
+        ceil_pts = sms * clk / cyc_pp
+        roof["request_bound"] = {"index_sectors_per_point": round(idx_pp, 3), "red_sectors_per_point": round(red_pp, 3),
+                                 "sm_cycles_per_point": round(cyc_pp, 3), "ceiling_points_per_s": round(ceil_pts, 1),
+                                 "kernel_points_per_s": round(n / (k_ms / 1e3), 1),
+                                 "frac": round(n / (k_ms / 1e3) / ceil_pts, 4),
+                                 "source": "profiles/round2/request_rates.json + " + os.path.relpath(prof, ROOT)}
     # ---- e2e: public API on pinned host buffers (rb_join_host), every step; ranks combine COUNT and SUM
     e2e = None
     if not a.no_e2e:

@@ -49,6 +49,10 @@ index = {}
 if ih + im > 0:
     index = {"index_l2_hit_rate": ih / (ih + im), "index_l1_hit_rate": lh / (lh + lm) if lh + lm else None,
              "index_l2_sectors_per_point": (ih + im) / npts if npts else None}
+    red = rawf("lts__t_sectors_srcunit_tex_op_red.sum")
+    if npts:
+        index["red_sectors_per_point"] = red / npts
+        summary["global REDs: L2 sectors per point"] = (f"{red / npts:.3f}", "")
     summary["index lookups: L2 hit rate"] = (f"{100 * ih / (ih + im):.2f}", "%")
     if lh + lm:
         summary["index lookups: L1 hit rate"] = (f"{100 * lh / (lh + lm):.2f}", "%")
