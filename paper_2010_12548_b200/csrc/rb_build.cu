@@ -1042,7 +1042,7 @@ static int index_impl(int L, int64_t total_cells, const int32_t* cp_in, const ui
   RB_CUDA(excl_scan_i64(psz.as<int64_t>(), poff.as<int64_t>(), npos + 1, s));
   int64_t npool = d2h(poff.as<int64_t>() + npos, s);
   if (npool >= (int64_t)RB_VALUE_PAYLOAD) return fail(RB_CAPACITY_ERROR, "owner pool exceeds 2^30 entries");
-  RB_CUDA(A->pool.alloc(std::max<int64_t>(npool, 1) * 4));
+  RB_CUDA(A->pool.alloc_persistent(std::max<int64_t>(npool, 1) * 4));
   A->pool_len = npool;
   RB_CUDA(pstart.alloc(std::max<int64_t>(npos, 1) * 8));
   RB_CUDA(plevel.alloc(std::max<int64_t>(npos, 1)));
@@ -1071,13 +1071,13 @@ static int index_impl(int L, int64_t total_cells, const int32_t* cp_in, const ui
     while (bits < std::min(2 * L, 29) && ((int64_t)1 << bits) < 2 * std::max<int64_t>(npos, 1)) ++bits;
     A->kshift = 2 * L - bits;
     const int64_t nslots = ((int64_t)1 << bits) + 1;
-    RB_CUDA(A->ktab.alloc(nslots * 4));
+    RB_CUDA(A->ktab.alloc_persistent(nslots * 4));
     k_key_table<<<nblk(nslots), 256, 0, s>>>(pstart.as<uint64_t>(), npos, A->kshift, nslots, A->ktab.as<uint32_t>());
     RB_CUDA(cudaGetLastError());
-    RB_CUDA(A->keys.alloc(std::max<int64_t>(npos, 1) * 16));
+    RB_CUDA(A->keys.alloc_persistent(std::max<int64_t>(npos, 1) * 16));
     if (npos) k_key_records<<<nblk(npos), 256, 0, s>>>(pstart.as<uint64_t>(), plevel.as<uint8_t>(), pval.as<uint32_t>(),
                                                        npos, A->keys.as<uint4>());
-    RB_CUDA(A->root.alloc(4));  // unused (no radix table levels)
+    RB_CUDA(A->root.alloc_persistent(4));  // unused (no radix table levels)
     RB_CUDA(cudaMemsetAsync(A->root.p, 0, 4, s));
     A->root_entries = 1;
     A->S = -1;
@@ -1086,7 +1086,7 @@ static int index_impl(int L, int64_t total_cells, const int32_t* cp_in, const ui
       if (const char* e = getenv("RB_SUMMARY_LEVEL")) Smax = std::min(atoi(e), 8);
       if (Smax >= 0 && 2 * (int64_t)A->n_regions + 1 < 0xffff) {
         const int S = std::min(Smax, L);
-        RB_CUDA(A->summary.alloc(((size_t)2 << (2 * S))));
+        RB_CUDA(A->summary.alloc_persistent(((size_t)2 << (2 * S))));
         k_key_summary<<<nblk((int64_t)1 << (2 * S)), 256, 0, s>>>(A->keys.as<uint4>(), npos, L, S,
                                                                   A->summary.as<uint16_t>());
         RB_CUDA(cudaGetLastError());
@@ -1155,7 +1155,7 @@ static int index_impl(int L, int64_t total_cells, const int32_t* cp_in, const ui
   A->T0 = T0;
   A->k = k;
   A->root_entries = (int64_t)1 << (2 * T0);
-  RB_CUDA(A->root.alloc(A->root_entries * 4));
+  RB_CUDA(A->root.alloc_persistent(A->root_entries * 4));
   RB_CUDA(cudaMemsetAsync(A->root.p, 0, A->root_entries * 4, s));
   IndexBuild B{};
   B.root = A->root.as<uint32_t>();
@@ -1202,7 +1202,7 @@ static int index_impl(int L, int64_t total_cells, const int32_t* cp_in, const ui
   int64_t total_nodes = 0, node_bytes = 0;
   for (int i = 0; i < B.nlev; ++i) {
     int64_t bytes = nnodes[i] * ((int64_t)4 << (2 * ks[i]));
-    RB_CUDA(node_bufs[i].alloc(std::max<int64_t>(bytes, 4)));
+    RB_CUDA(node_bufs[i].alloc_persistent(std::max<int64_t>(bytes, 4)));
     RB_CUDA(cudaMemsetAsync(node_bufs[i].p, 0, std::max<int64_t>(bytes, 4), s));
     B.nodes[i] = node_bufs[i].as<uint32_t>();
     total_nodes += nnodes[i];
@@ -1258,8 +1258,8 @@ static int index_impl(int L, int64_t total_cells, const int32_t* cp_in, const ui
     RB_CUDA(cudaGetLastError());
     RB_CUDA(excl_scan_u32(esc.as<uint32_t>(), eoff.as<uint32_t>(), nblocks + 1, s));
     const int64_t nwide = d2h(eoff.as<uint32_t>() + nblocks, s);
-    RB_CUDA(A->pblk.alloc(std::max<int64_t>(nblocks, 1) * 16));
-    RB_CUDA(A->pwide.alloc(std::max<int64_t>(nwide, 1) * 64));
+    RB_CUDA(A->pblk.alloc_persistent(std::max<int64_t>(nblocks, 1) * 16));
+    RB_CUDA(A->pwide.alloc_persistent(std::max<int64_t>(nwide, 1) * 64));
     if (nblocks)
       k_pack_emit<<<nblk(nblocks), 256, 0, s>>>(node_bufs[1].as<uint32_t>(), nblocks, pd, eoff.as<uint32_t>(),
                                                 A->pblk.as<uint4>(), A->pwide.as<uint32_t>());
@@ -1285,8 +1285,8 @@ static int index_impl(int L, int64_t total_cells, const int32_t* cp_in, const ui
     RB_CUDA(cudaGetLastError());
     RB_CUDA(excl_scan_u32(esc.as<uint32_t>(), eoff.as<uint32_t>(), nblocks + 1, s));
     const int64_t nwide = d2h(eoff.as<uint32_t>() + nblocks, s);
-    RB_CUDA(A->pblk.alloc(std::max<int64_t>(nblocks, 1) * 16));
-    RB_CUDA(A->pwide.alloc(std::max<int64_t>(nwide, 1) * 64));
+    RB_CUDA(A->pblk.alloc_persistent(std::max<int64_t>(nblocks, 1) * 16));
+    RB_CUDA(A->pwide.alloc_persistent(std::max<int64_t>(nwide, 1) * 64));
     if (nblocks)
       k_pack_emit<<<nblk(nblocks), 256, 0, s>>>(node_bufs[0].as<uint32_t>(), nblocks, pd, eoff.as<uint32_t>(),
                                                 A->pblk.as<uint4>(), A->pwide.as<uint32_t>());
@@ -1313,7 +1313,7 @@ static int index_impl(int L, int64_t total_cells, const int32_t* cp_in, const ui
     A->S = -1;
     if (Smax >= 0 && 2 * (int64_t)A->n_regions + 1 < 0xffff) {
       const int S = std::min(Smax, T0);
-      RB_CUDA(A->summary.alloc(((size_t)2 << (2 * S))));
+      RB_CUDA(A->summary.alloc_persistent(((size_t)2 << (2 * S))));
       k_summary<<<nblk(((int64_t)32 << (2 * S))), 256, 0, s>>>(A->root.as<uint32_t>(), T0, S, A->summary.as<uint16_t>());
       RB_CUDA(cudaGetLastError());
       A->S = S;
@@ -1757,7 +1757,7 @@ extern "C" int rb_approx_set_hot(rb_approx* a, const int32_t* regions, int32_t n
       if (seen[r]++) return fail(RB_CONFIG_ERROR, "duplicate hot region");
     }
   }
-  RB_CUDA(a->hot_region.alloc(n_hot * 4));
+  RB_CUDA(a->hot_region.alloc_persistent(n_hot * 4));
   RB_CUDA(cudaMemcpyAsync(a->hot_region.p, h.data(), n_hot * 4, cudaMemcpyHostToDevice, s));
   DBuf remap;
   RB_CUDA(remap.alloc((size_t)a->n_regions * 4));

@@ -223,6 +223,14 @@ struct DBuf {
     pooled = false;
     return cudaMalloc(&p, b);
   }
+  // index data that outlives the build: plain cudaMalloc, so the pool holds only build scratch and its
+  // working set (and so the build time) stays the same from one build to the next
+  cudaError_t alloc_persistent(size_t b) {
+    release();
+    bytes = b;
+    pooled = false;
+    return b ? cudaMalloc(&p, b) : cudaSuccess;
+  }
   void detach() { pooled = false; }  // outlives the allocating stream: cudaFree later (synchronising)
   template <class T> T* as() const { return (T*)p; }
 };

@@ -1,7 +1,6 @@
-timeout 900 python -m pytest tests/test_gpu_packed.py tests/test_gpu_scale.py -q -x -k "not c3" 2>&1 | tail -3
-for r in 1 2; do
-timeout 300 python tools/profile_pass.py c4 200000000 trie 3 12 2>&1 | grep -E "Gpts" | tail -1 | sed "s/^/TRIE12 /"
-RB_PK3_CFG=0 timeout 300 python tools/profile_pass.py c4 200000000 packed 3 12 2>&1 | grep -E "Gpts" | tail -1 | sed "s/^/PKL12 cfg0 /"
-RB_PK3_CFG=1 timeout 300 python tools/profile_pass.py c4 200000000 packed 3 12 2>&1 | grep -E "Gpts" | tail -1 | sed "s/^/PKL12 cfg1 /"
-timeout 300 python tools/profile_pass.py c4 200000000 packed 3 13 2>&1 | grep -E "Gpts" | tail -1 | sed "s/^/PK2-13 /"
+for spec in "c4 trie -1" "c4 packed -1" "c2 trie -1"; do
+  set -- $spec
+  RB_BUILD_TRACE=1 timeout 600 python tools/build_time.py $1 $2 $3 6 2> gpurun_out/r2_build4_$1_$2.trace | tail -1
 done
+timeout 900 python -m pytest tests/test_gpu_api.py tests/test_gpu_packed.py -q -x 2>&1 | tail -2
+timeout 900 python bench.py --steps 5 --warmup 3 --no-cpu > gpurun_out/r2_bench_pin.json 2> gpurun_out/r2_bench_pin.err; echo bench rc=$?
