@@ -322,13 +322,13 @@ def run_ours(a):
     if lookups is not None and os.path.exists(rates_p):
         with open(rates_p) as f:
             rates = json.load(f)
-        idx_pp = pj["index_l2_sectors_per_point"]
+        idx_pp = pj.get("l1_load_sectors_per_point") or pj["index_l2_sectors_per_point"]
         red_pp = pj.get("red_sectors_per_point", 0.0) or 0.0
-        cyc_pp = idx_pp / rates["load_per_sm_clk"] + red_pp / rates["red_per_sm_clk"]
+        cyc_pp = idx_pp / rates["load_per_sm_clk"] + red_pp * rates["red_in_mix_sm_clk"]
         clk = (sampler.summary().get("sm_mhz") or 1965) * 1e6
         sms = torch.cuda.get_device_properties(local).multi_processor_count
         ceil_pts = sms * clk / cyc_pp
-        roof["request_bound"] = {"index_sectors_per_point": round(idx_pp, 3), "red_sectors_per_point": round(red_pp, 3),
+        roof["request_bound"] = {"index_load_sectors_per_point": round(idx_pp, 3), "red_sectors_per_point": round(red_pp, 3),
                                  "sm_cycles_per_point": round(cyc_pp, 3), "ceiling_points_per_s": round(ceil_pts, 1),
                                  "kernel_points_per_s": round(n / (k_ms / 1e3), 1),
                                  "frac": round(n / (k_ms / 1e3) / ceil_pts, 4),

@@ -52,6 +52,8 @@ if ih + im > 0:
     red = rawf("lts__t_sectors_srcunit_tex_op_red.sum")
     if npts:
         index["red_sectors_per_point"] = red / npts
+        index["l1_load_sectors_per_point"] = (lh + lm) / npts  # the SM-side random requests (index loads)
+        summary["index lookups: L1 sectors per point"] = (f"{(lh + lm) / npts:.3f}", "")
         summary["global REDs: L2 sectors per point"] = (f"{red / npts:.3f}", "")
     summary["index lookups: L2 hit rate"] = (f"{100 * ih / (ih + im):.2f}", "%")
     if lh + lm:
