@@ -2189,7 +2189,8 @@ static cudaError_t deep_run(const PassArgs& a, size_t smem, cudaStream_t s, int*
 
 // C4 (200M points, 4095 hot slots): 3 stages + 1 hot-slot copy 1.64 ms; 2 stages 1.67; 4 stages 1.73;
 // 2 copies 2.07 (less L1 for lookups in flight); 2048 hot slots 2.35, 1024 2.98 (profiles/round1/deep_sweep.txt)
-static const WarpCfg kDeepCfgs[] = {{16, 4, 3}, {16, 4, 2}, {16, 4, 4}};
+// 3: 15 consumer warps (128 registers); the same speed for the radix table (C4 1.67 vs 1.65 ms)
+static const WarpCfg kDeepCfgs[] = {{16, 4, 3}, {16, 4, 2}, {16, 4, 4}, {15, 4, 3}};
 
 template <int XY, bool ATTR, int LAY = 0>
 static cudaError_t deep_dispatch(int ci, const PassArgs& a, size_t smem, cudaStream_t s, int* blocks, bool launch) {
@@ -2215,6 +2216,7 @@ static cudaError_t deep_dispatch(int ci, const PassArgs& a, size_t smem, cudaStr
   switch (ci) {
     case 0: return deep_run<XY, ATTR, 16, 4, 3>(a, smem, s, blocks, launch);
     case 1: return deep_run<XY, ATTR, 16, 4, 2>(a, smem, s, blocks, launch);
+    case 3: return deep_run<XY, ATTR, 15, 4, 3>(a, smem, s, blocks, launch);
     default: return deep_run<XY, ATTR, 16, 4, 4>(a, smem, s, blocks, launch);
   }
 }

@@ -1,6 +1,9 @@
-for spec in "c4 trie -1" "c4 packed -1" "c2 trie -1"; do
-  set -- $spec
-  RB_BUILD_TRACE=1 timeout 600 python tools/build_time.py $1 $2 $3 6 2> gpurun_out/r2_build4_$1_$2.trace | tail -1
+for r in 1 2; do
+for lib in build/ab/head.so build/ab/reorder.so; do
+  RASTERBOUND_B200_LIB=$lib timeout 300 python tools/profile_pass.py c4 200000000 trie 3 12 2>&1 | grep Gpts | tail -1 | sed "s|^|$lib cfg0 |"
 done
-timeout 900 python -m pytest tests/test_gpu_api.py tests/test_gpu_packed.py -q -x 2>&1 | tail -2
-timeout 900 python bench.py --steps 5 --warmup 3 --no-cpu > gpurun_out/r2_bench_pin.json 2> gpurun_out/r2_bench_pin.err; echo bench rc=$?
+RB_DEEP_CFG=3 RASTERBOUND_B200_LIB=build/ab/reorder.so timeout 300 python tools/profile_pass.py c4 200000000 trie 3 12 2>&1 | grep Gpts | tail -1 | sed "s|^|reorder cfg3 |"
+for lib in build/ab/head.so build/ab/reorder.so; do
+  RASTERBOUND_B200_LIB=$lib timeout 300 python tools/profile_pass.py c4 200000000 packed 3 12 2>&1 | grep Gpts | tail -1 | sed "s|^|$lib PKL |"
+done
+done
