@@ -38,7 +38,8 @@ def main():
             rep = validate_full(idx, xy, w.epsilon)
             el = time.perf_counter() - t
             d = rep.as_dict()
-            d.update(workload=w.name, mode=["CONSERVATIVE", "LIBERAL"][mode], max_level=L, seconds=round(el, 3),
+            d.update(workload=w.name, mode=["CONSERVATIVE", "CENTER_SAMPLED"][mode], max_level=L, seconds=round(el, 3),
+                     grid=w.meta.get("grid", "ingest"), leaf_side=w.grid.extent / (1 << L),
                      polygons=packed.n_polygons, regions=packed.n_regions)
             print(json.dumps(d), flush=True)
             del idx
