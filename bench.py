@@ -85,8 +85,6 @@ def _free_port() -> int:
 def relaunch(a) -> int:
     """`--gpus N` outside torchrun: run this script under torch.distributed.run with N ranks (one per GPU)."""
     env = dict(os.environ)
-    env.setdefault("NCCL_DEBUG", "INFO")  # NCCL reports its transport / algorithm choices
-    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT,TUNING")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
            "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
     return subprocess.call(cmd, env=env)
@@ -142,6 +140,25 @@ def repo_libs() -> list:
     except OSError:
         pass
     return sorted(out)
+
+
+def nccl_summary(path, world):
+    """What NCCL_DEBUG=INFO recorded for this rank's communicator (None for one rank)."""
+    if world <= 1:
+        return None
+    out = {"ranks": world, "debug_file": path}
+    try:
+        with open(path) as f:
+            lines = f.read().splitlines()
+    except (OSError, TypeError):
+        out["note"] = "no NCCL debug file (NCCL_DEBUG_FILE set by the caller)"
+        return out
+    out["lines"] = len(lines)
+    out["version"] = next((l.split("NCCL version", 1)[1].strip() for l in lines if "NCCL version" in l), None)
+    out["nvls"] = any("NVLS" in l and ("comm" in l or "enabled" in l.lower() or "NVLS multicast" in l) for l in lines)
+    out["p2p_nvlink"] = any("via P2P" in l or "P2P/CUMEM" in l or "NVL" in l for l in lines)
+    out["init_lines"] = [l.split("NCCL INFO", 1)[-1].strip()[:160] for l in lines if "comm" in l and "rank" in l][:4]
+    return out
 
 
 def peaks():
@@ -242,7 +259,15 @@ def run_ours(a):
     if world != a.gpus:
         raise SystemExit(f"bench.py: --gpus {a.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
+    nccl_log = None
     if world > 1:
+        # NCCL's own account of the communicator (ranks, transports, NVLS), to a per-rank file so that
+        # stdout keeps the one JSON line; rank 0 summarises its file in that line
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,TUNING")
+        if "NCCL_DEBUG_FILE" not in os.environ:
+            nccl_log = os.path.join(os.environ.get("TMPDIR", "/tmp"), f"rb_bench_nccl.{os.getpid()}.r{rank}.log")
+            os.environ["NCCL_DEBUG_FILE"] = nccl_log
         dist.init_process_group("nccl", init_method="env://", device_id=torch.device("cuda", local))
     C = CONFIGS[a.config]
     n = a.points or C["points"]
@@ -404,6 +429,7 @@ def run_ours(a):
                       "build_ms_runs": [round(x, 1) for x in warm_ms], "build_ms_first": round(st["build_ms"], 1)},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": sampler.summary(), "parity_vs_oracle": parity, "libs_loaded": repo_libs(),
+            "nccl": nccl_summary(nccl_log, world),
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -465,8 +491,7 @@ def run_reference(a):
 
 def spawn_check(a):
     rank, world, local = dist_env()
-    line = json.dumps({"rank": rank, "world": world, "local_rank": local, "gpus": a.gpus,
-                       "nccl_debug": os.environ.get("NCCL_DEBUG")}) + "\n"
+    line = json.dumps({"rank": rank, "world": world, "local_rank": local, "gpus": a.gpus}) + "\n"
     sys.stdout.flush()
     os.write(1, line.encode())  # one write per rank: ranks share the pipe
 

@@ -221,3 +221,32 @@ def test_float64_attribute_is_summed_in_two_parts(oracle_lib):
     np.testing.assert_allclose(r.sum.cpu().numpy(), exact, rtol=1e-6, atol=1e-9)
     f32_only = idx.point_pass(torch.as_tensor(xy).cuda(), torch.as_tensor(hi).cuda()).sum.cpu().numpy()
     assert np.max(np.abs(r.sum.cpu().numpy() - exact)) < np.max(np.abs(f32_only - exact))
+
+
+def test_spec_literal_tier_float64_mixed_sign_sums():
+    """the SPEC-literal tier (float64 attribute values, Python float
+    accumulation) checks a float64, mixed-sign SUM: the device result lies within
+    2^-21 * sum |w| of it (the float64 attribute takes the two-part path)."""
+    torch = _gpu()
+    from oracle import spec_literal as SL
+    from paper_2010_12548_b200.engine import ApproxIndex
+    from paper_2010_12548_b200.geometry import pack_regions
+
+    regions = random_polygons(17, k=6, holes=True)
+    L = 7
+    grid = UNIT.with_level(L)
+    rng = np.random.default_rng(3)
+    xy = rng.random((20_000, 2))
+    w = rng.normal(0.0, 1e6, len(xy)) + rng.random(len(xy)) * 1e-3  # float64, mixed sign, not float32-exact
+    trie, _ = SL.build([(r.id, [p.rings]) for r in regions for p in [r.geometry]], (0.0, 0.0), 1.0, L)
+    ref = SL.join_act(xy.tolist(), trie, (0.0, 0.0), 1.0, w.tolist())
+    ref_abs = SL.join_act(xy.tolist(), trie, (0.0, 0.0), 1.0, np.abs(w).tolist())
+    idx = ApproxIndex(pack_regions(regions), grid, 0, layout="trie")
+    r = idx.point_pass(torch.as_tensor(xy).cuda(), torch.as_tensor(w).cuda()).check()
+    cnt, sm = r.cnt.cpu().numpy(), r.sum.cpu().numpy()
+    for k, reg in enumerate(regions):
+        a = ref.get(reg.id, [0, 0, 0.0, 0.0])
+        b = ref_abs.get(reg.id, [0, 0, 0.0, 0.0])
+        assert (cnt[k, 0], cnt[k, 1]) == (a[0], a[1])
+        assert abs(sm[k, 0] - a[2]) <= FIXED_POINT_REL * b[2] + 1e-9
+        assert abs(sm[k, 1] - a[3]) <= FIXED_POINT_REL * b[3] + 1e-9
