@@ -39,7 +39,8 @@ CONFIGS = {
                         "uniform raster, COUNT", points=1_000_000, bpp=16, dtype="f64", agg="COUNT"),
     "c2": dict(workload="C2 city-scale: 100M f64 points (50-Gaussian mixture + 10% uniform over 40x40 km), "
                         "fare f32, 260 jittered-Voronoi tiling polygons (100-500 vertices), eps=4.9 m, "
-                        "uniform raster, COUNT + SUM(fare)", points=100_000_000, bpp=20, dtype="f64",
+                        "uniform raster (evaluated through the radix-table index: the same leaf owners as the dense "
+                        "uniform grid, SPEC.md:248), COUNT + SUM(fare)", points=100_000_000, bpp=20, dtype="f64",
                agg="SUM:fare"),
     "c4": dict(workload="C4 fine-polygon: 1B f32-offset points (same mixture over 100x100 km), fare f32, 40,000 "
                         "jittered-Voronoi polygons (10-30 vertices), eps=1 m, hierarchical raster (coarse interior "

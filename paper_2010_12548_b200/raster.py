@@ -162,6 +162,9 @@ def rasterize_uniform(poly, cfg: GridConfig, epsilon: float, mode: RasterMode = 
     return expand_uniform(rasterize_hierarchical(poly, cfg, epsilon, mode, region_id))
 
 
+_CLASSIFY_CACHE: dict = {}
+
+
 def classify_cell(c: CellId, poly: Polygon, cfg: GridConfig | None = None) -> CellClass:
     """INSIDE / OUTSIDE / PARTIAL for a cell of the grid `cfg`
     (default: unit square at origin).  PARTIAL iff the boundary meets the open
@@ -170,7 +173,15 @@ def classify_cell(c: CellId, poly: Polygon, cfg: GridConfig | None = None) -> Ce
 
     cfg = cfg or GridConfig(Point2D(0.0, 0.0), 1.0, 0)
     grid = cfg.with_level(c.level)
-    idx = ApproxIndex(pack_regions([RegionRecord(0, poly)]), grid, N.MODE_CONSERVATIVE, layout="trie")
+    key = (id(poly), grid.origin.x, grid.origin.y, grid.extent, c.level)
+    hit = _CLASSIFY_CACHE.get(key)
+    if hit is not None and hit[0] is poly:
+        idx = hit[1]
+    else:  # one index per (polygon, grid level), reused by further cells of that polygon
+        idx = ApproxIndex(pack_regions([RegionRecord(0, poly)]), grid, N.MODE_CONSERVATIVE, layout="trie")
+        if len(_CLASSIFY_CACHE) >= 8:
+            _CLASSIFY_CACHE.pop(next(iter(_CLASSIFY_CACHE)))
+        _CLASSIFY_CACHE[key] = (poly, idx)
     ix, iy = _decode(c)
     side = grid.side()
     centre = np.array([[cfg.origin.x + (ix + 0.5) * side, cfg.origin.y + (iy + 0.5) * side]])
