@@ -1,9 +1,4 @@
-for r in 1 2; do
-for lib in build/ab/head.so build/ab/reorder.so; do
-  RASTERBOUND_B200_LIB=$lib timeout 300 python tools/profile_pass.py c4 200000000 trie 3 12 2>&1 | grep Gpts | tail -1 | sed "s|^|$lib cfg0 |"
-done
-RB_DEEP_CFG=3 RASTERBOUND_B200_LIB=build/ab/reorder.so timeout 300 python tools/profile_pass.py c4 200000000 trie 3 12 2>&1 | grep Gpts | tail -1 | sed "s|^|reorder cfg3 |"
-for lib in build/ab/head.so build/ab/reorder.so; do
-  RASTERBOUND_B200_LIB=$lib timeout 300 python tools/profile_pass.py c4 200000000 packed 3 12 2>&1 | grep Gpts | tail -1 | sed "s|^|$lib PKL |"
-done
-done
+timeout 2400 python -m pytest tests -q -m gpu 2>&1 | tail -4
+timeout 900 python bench.py > gpurun_out/r2_bench_final2.json 2> gpurun_out/r2_bench_final2.err; echo bench rc=$?
+timeout 900 python bench.py --config c2 > gpurun_out/r2_bench_c2_final.json 2> gpurun_out/r2_bench_c2_final.err; echo bench c2 rc=$?
+timeout 600 python bench.py --impl reference > gpurun_out/r2_bench_ref.json 2> gpurun_out/r2_bench_ref.err; echo ref rc=$?
