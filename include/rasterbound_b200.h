@@ -139,7 +139,9 @@ int rb_approx_stats(const rb_approx* a, rb_stats* out);
  * alpha COUNT/SUM the point pass privatises in shared memory when the full
  * per-region histogram does not fit there (large region sets, e.g. 40,000
  * census blocks).  Results are unchanged.  At most rb_stats.max_hot regions: 2^(30 - b) - 1 (capped at
- * 16383) where b = max(16, bit length of 2 * n_regions) is the width of the owner codes. */
+ * 16383) where b = max(16, bit length of 2 * n_regions) is the width of the owner codes.  Rewrites the
+ * index's owner values in place, once (a second call is RB_CONFIG_ERROR): call it before, not during,
+ * concurrent point passes (the Python layer does so under a lock on the first pass). */
 int rb_approx_set_hot(rb_approx* a, const int32_t* regions, int32_t n_hot, void* stream);
 void rb_approx_free(rb_approx* a);
 

@@ -1,4 +1,2 @@
-timeout 2400 python -m pytest tests -q -m gpu 2>&1 | tail -4
-timeout 900 python bench.py > gpurun_out/r2_bench_final2.json 2> gpurun_out/r2_bench_final2.err; echo bench rc=$?
-timeout 900 python bench.py --config c2 > gpurun_out/r2_bench_c2_final.json 2> gpurun_out/r2_bench_c2_final.err; echo bench c2 rc=$?
-timeout 600 python bench.py --impl reference > gpurun_out/r2_bench_ref.json 2> gpurun_out/r2_bench_ref.err; echo ref rc=$?
+timeout 1800 python tools/parity_full.py c4 gpurun_out/r2_parity_c4.jsonl > gpurun_out/r2_parity.log 2>&1; echo parity rc=$?
+timeout 1800 python tools/sweep_c3.py 100000000 gpurun_out/r2_c3_sweep.jsonl > gpurun_out/r2_c3.log 2>&1; echo c3 rc=$?

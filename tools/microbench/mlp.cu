@@ -74,7 +74,7 @@ static void run(const uint32_t* tab, size_t mb, int warps, int pad_kb, int sms, 
   if (smem > 227 * 1024) return;
   auto kern = k<MODE, PPT>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-  const uint32_t mask16 = (uint32_t)((mb << 20) / 16 - 1);
+  const uint32_t mask16 = (uint32_t)((getenv("MLP_KB") ? (mb << 10) : (mb << 20)) / 16 - 1);  // MLP_KB: sizes in KB
   const int iters = 400;
   kern<<<sms, threads, smem>>>(tab, mask16, iters, out);
   cudaEvent_t a, b;
@@ -106,6 +106,14 @@ int main() {
   cudaMemset(tab, 1, maxmb << 20);
   cudaMalloc(&out, 16 + 80000 * 8);
   const char* sweep = getenv("MLP_SWEEP");
+  if (sweep && sweep[0] == '4') {  // L1-resident tables (MLP_KB=1): is the 1/clk limit the L1 or the L2?
+    for (size_t kb : {16ul, 64ul, 256ul, 32768ul})
+      for (int warps : {16}) {
+        run<0, 8>(tab, kb, warps, 0, sms, clk, out);
+        run<1, 8>(tab, kb, warps, 0, sms, clk, out);
+      }
+    return 0;
+  }
   if (sweep && sweep[0] == '3') {  // REDs alone and mixed with loads (L2-resident table)
     for (int warps : {8, 16})
       for (int pad : {0, 128}) {
