@@ -1,5 +1,6 @@
 """Randomised parity against the oracle: random (possibly overlapping, holed)
-polygons, random grid levels, both modes, all three index layouts, f64/f32
+polygons, random grid levels, both modes, every index layout (radix table, sorted keys, dense grid, packed
+in both forms), f64/f32
 points drawn uniformly, clustered, on grid lines and on polygon vertices,
 attributes spanning many magnitudes (zero, negative, out of the fixed-point
 window).  COUNT must be bit-exact, SUM within rel 1e-6.  Prints one line per
@@ -39,7 +40,8 @@ for c in range(cases):
         regions = random_polygons(int(seed0 + c), int(rng.integers(3, 40)), holes=(kind == "holes"))
         L = int(rng.integers(3, 22))  # up to 21: beyond the ring kernels' 2^20 window
     mode = int(rng.integers(0, 2))
-    layouts = ["trie", "keys"] + (["dense"] if L <= 12 else [])
+    layouts = [("trie", -1), ("keys", -1), ("packed", -1)] + ([("packed", L - 3)] if L >= 3 else []) + \
+        ([("dense", -1)] if L <= 12 else [])
     grid = GridConfig(Point2D(0.0, 0.0), 1.0, L)
     n = int(rng.integers(1, 300_000))
     parts = [rng.random((n, 2))]
@@ -59,8 +61,8 @@ for c in range(cases):
     hot = None
     if kind == "big" and rng.random() < 0.5:  # an explicit hot subset: cold regions take the global REDs
         hot = np.sort(rng.choice(p.n_regions, int(rng.integers(0, min(4095, p.n_regions))), replace=False))
-    for layout in layouts:
-        idx = ApproxIndex(p, grid, mode, layout=layout)
+    for layout, rl in layouts:
+        idx = ApproxIndex(p, grid, mode, layout=layout, root_level=rl)
         if hot is not None:
             idx.set_hot(hot)
         for pts, at in ((xy, attr), (xy.astype(np.float32), None)):
@@ -77,10 +79,11 @@ for c in range(cases):
                 ok = ok and np.allclose(s, sum_o, rtol=1e-6, atol=1e-6 * np.abs(attr).max())
             if not ok:
                 fails += 1
-                print(f"FAIL case {c} seed {seed0 + c}: {kind} R={p.n_regions} L={L} mode={mode} layout={layout} "
+                print(f"FAIL case {c} seed {seed0 + c}: {kind} R={p.n_regions} L={L} mode={mode} layout={layout}/{rl} "
                       f"n={len(pts)} f32={pts.dtype == np.float32} count_diff={int(np.abs(cnt - cnt_o).sum())}",
                       flush=True)
         del idx
-    print(f"case {c}: {kind} R={p.n_regions} L={L} mode={mode} n={len(xy)} layouts={layouts} ok", flush=True)
+    print(f"case {c}: {kind} R={p.n_regions} L={L} mode={mode} n={len(xy)} layouts={[x for x, _ in layouts]} ok",
+          flush=True)
 print(f"{cases} cases, {fails} mismatches, {time.time() - t0:.0f} s")
 sys.exit(1 if fails else 0)

@@ -1,2 +1,3 @@
-timeout 1800 python tools/parity_full.py c4 gpurun_out/r2_parity_c4.jsonl > gpurun_out/r2_parity.log 2>&1; echo parity rc=$?
-timeout 1800 python tools/sweep_c3.py 100000000 gpurun_out/r2_c3_sweep.jsonl > gpurun_out/r2_c3.log 2>&1; echo c3 rc=$?
+timeout 2400 python tools/fuzz_parity.py 150 5000 > gpurun_out/r2_fuzz1.log 2>&1; echo fuzz1 rc=$?
+timeout 1800 python tools/fuzz_parity.py 40 7000 big > gpurun_out/r2_fuzz2.log 2>&1; echo fuzz2 rc=$?
+tail -2 gpurun_out/r2_fuzz1.log gpurun_out/r2_fuzz2.log
