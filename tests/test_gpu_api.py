@@ -101,6 +101,9 @@ def test_act_duplicate_cells_idempotent_and_widths():
     ref = A.act_lookup_many(A.act_build(covers), xy)
     for w in (2, 4):
         assert A.act_lookup_many(A.act_build(covers + covers[:3], radix_width=w, root_level=0), xy) == ref
+    # every index layout the engine has is reachable from act_build (keys was not)
+    for layout in ("dense", "keys", "packed"):
+        assert A.act_lookup_many(A.act_build(covers + covers[:3], layout=layout), xy) == ref, layout
 
 
 @pytest.mark.parametrize("engine", ["act", "canvas"])
