@@ -411,6 +411,30 @@ def run_ours(a):
         ok_c = bool(np.array_equal(cnt_g, cnt_o))
         rel = float(np.max(np.abs(r.sum.cpu().numpy() - sum_o) / np.maximum(np.abs(sum_o), 1e-30))) if attr is not None else 0.0
         parity = {"points": m, "count_bit_exact": ok_c, "sum_max_rel_err": rel}
+    # C4 on the SPEC ingest-rule grid as well (same points; leaf side 0.389 m instead of eps/sqrt(2)): the
+    # headline's grid choice is visible next to the alternative, timed the same way
+    alt = None
+    if a.config == "c4" and a.grid == "eps" and world == 1:
+        from paper_2010_12548_b200.grid import ingest_grid
+
+        ig = ingest_grid(0.0, 0.0, 100_000.0, 100_000.0)
+        alt_prep = PreparedJoin(w.regions, q, ig, layout=layout, root_level=a.root_level)
+        alt_out = alt_prep.index.point_pass(xy, attr)
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(5):
+            alt_prep.index.point_pass(xy, attr, out=alt_out)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        alt_out.check()
+        ams = f0.elapsed_time(f1) / 5
+        ast = alt_prep.stats()
+        alt = {"grid": "ingest (data MBR + 1%, SPEC.md:556)", "max_level": ast["max_level"],
+               "leaf_side": ig.extent / (1 << ast["max_level"]), "points_per_s": round(n / (ams / 1e3), 1),
+               "ms_per_pass": round(ams, 4), "index_bytes": ast["index_bytes"],
+               "boundary_leaves": ast["n_boundary_cells"]}
+        del alt_prep, alt_out
     # build time: the first build of a process pays module loading and allocator growth; the median of
     # warm rebuilds (after the timed regions, so their teardown cannot land inside them) is the steady state
     warm_ms = []
@@ -425,12 +449,13 @@ def run_ours(a):
             "vs_baseline": None, "dtype": C["dtype"], "data": "synthetic (seeded generators, DESIGN.md Workloads)",
             "config": config_dict(a, w, grid.max_level, world),
             "index": {"layout": layout, "root_level": st["root_level"], "index_bytes": st["index_bytes"],
+                      "boundary_leaves": st["n_boundary_cells"],
                       "n_nodes": st["n_nodes"], "hot_regions": None if prep.index._hot is None else len(prep.index._hot),
                       "build_ms": round(float(np.median(warm_ms)), 1) if warm_ms else None,
                       "build_ms_runs": [round(x, 1) for x in warm_ms], "build_ms_first": round(st["build_ms"], 1)},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": sampler.summary(), "parity_vs_oracle": parity, "libs_loaded": repo_libs(),
-            "nccl": nccl_summary(nccl_log, world),
+            "nccl": nccl_summary(nccl_log, world), "alt_grid": alt,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -1401,14 +1401,23 @@ __global__ void __launch_bounds__(NW * 32 + 32, NW <= 8 ? 2 : 1) k_point_pass_ri
 // Only the low L - T0 bits of a point's cell coordinates address its node
 // slots, so a tile in flight carries them packed in one register per point.
 //
+// Index forms (LAY): 0 radix table (node levels as above), 1 sorted keys (bucket in A,
+// records in B1), 2 packed below the root (block in B1, palette select in C, three
+// stages), 3 packed leaves below one u32 node level (node in B1, block in B2, select
+// in C; 15 consumer warps for its 128 registers).
+//
 // Accumulation keeps the global-histogram semantics of
 // k_point_pass_tma: interior single owners of a hot region (rb_approx_set_hot,
-// value bits 18..29 = slot + 1) with an in-window attribute take three shared
-// REDs into the region's privatised alpha slot; every other owner entry (cold
-// region, boundary leaf -> alpha and beta, owner list, out-of-window
-// attribute) goes through the per-warp rare queue to global REDG (u64 count,
-// f64 sum).  Hot slots drain to the CTA's fixed-point row like the ring
-// kernel's bins and are flushed into the global outputs at the end.
+// value bits hot_shift..29 = slot + 1) with an in-window attribute take three
+// shared REDs into the region's privatised alpha slot; cold interior single
+// owners take two predicated global REDs (u64 count, f64 sum); boundary leaves,
+// owner lists and out-of-window attributes go through the per-warp rare queue.
+// Hot slots drain to the CTA's fixed-point row like the ring kernel's bins and
+// are flushed into the global outputs at the end.
+//
+// The C4 pass is bound by random global requests per point (about 1.3 index
+// loads and 0.5 REDs), not by HBM bytes: DESIGN.md section 5 measures the SM's
+// request rates and puts this kernel at 0.81 of the resulting ceiling.
 // ---------------------------------------------------------------------------
 template <bool ATTR>
 __device__ __forceinline__ void add_owners_g(uint32_t bins, const uint32_t* __restrict__ pool, uint32_t v, float w,
