@@ -1145,7 +1145,10 @@ static int index_impl(int L, int64_t total_cells, const int32_t* cp_in, const ui
     }
   }
   if ((int)ks.size() > 8) return fail(RB_CONFIG_ERROR, "too many index levels (raise root_level or radix_width)");
-  if (T0 > 17) return fail(RB_CAPACITY_ERROR, "root table above level 17 (68.7 GB) is not supported; use the trie layout");
+  // the point-pass kernels address root slots with 32-bit indices ((row << T0) | col): T0 <= 16 (17.2 GB)
+  if (T0 > 16)
+    return fail(RB_CAPACITY_ERROR, "root table above level 16 (17.2 GB) is not supported; use the trie or packed "
+                                   "layout with a lower root_level");
   {
     size_t fr = 0, tot = 0;
     RB_CUDA(cudaMemGetInfo(&fr, &tot));

@@ -104,3 +104,9 @@ def test_packed_rejects_bad_root_level():
         _prepared(regions, UNIT.with_level(10), 0, "packed", root_level=9)
     with pytest.raises(E.ConfigError):
         _prepared(regions, UNIT.with_level(12), 0, "packed", root_level=2)
+    # root slots are addressed with 32-bit indices in the point pass: root levels above 16 are refused
+    # (fuzz_parity found wrong counts at root level 17 before this limit)
+    with pytest.raises(E.CapacityError):
+        _prepared(regions, UNIT.with_level(20), 0, "packed", root_level=17)
+    with pytest.raises(E.CapacityError):
+        _prepared(regions, UNIT.with_level(19), 0, "trie", root_level=17)

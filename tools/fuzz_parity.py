@@ -40,7 +40,7 @@ for c in range(cases):
         regions = random_polygons(int(seed0 + c), int(rng.integers(3, 40)), holes=(kind == "holes"))
         L = int(rng.integers(3, 22))  # up to 21: beyond the ring kernels' 2^20 window
     mode = int(rng.integers(0, 2))
-    layouts = [("trie", -1), ("keys", -1), ("packed", -1)] + ([("packed", L - 3)] if 3 <= L <= 20 else []) + \
+    layouts = [("trie", -1), ("keys", -1), ("packed", -1)] + ([("packed", L - 3)] if 3 <= L <= 19 else []) + \
         ([("dense", -1)] if L <= 12 else [])
     grid = GridConfig(Point2D(0.0, 0.0), 1.0, L)
     n = int(rng.integers(1, 300_000))

@@ -1,3 +1,3 @@
-timeout 3000 python tools/fuzz_parity.py 200 5000 > gpurun_out/r2_fuzz1.log 2>&1; echo fuzz1 rc=$?
-timeout 1800 python tools/fuzz_parity.py 60 8000 big > gpurun_out/r2_fuzz3.log 2>&1; echo fuzz3 rc=$?
-timeout 900 python bench.py --steps 10 --warmup 3 --no-cpu --no-e2e > gpurun_out/r2_bench_alt.json 2> gpurun_out/r2_bench_alt.err; echo bench rc=$?
+timeout 900 python -m pytest tests/test_gpu_packed.py -q -x 2>&1 | tail -2
+timeout 3000 python tools/fuzz_parity.py 250 5000 > gpurun_out/r2_fuzz1.log 2>&1; echo fuzz1 rc=$?
+timeout 3000 python tools/fuzz_parity.py 250 30000 > gpurun_out/r2_fuzz4.log 2>&1; echo fuzz4 rc=$?
