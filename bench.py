@@ -66,7 +66,7 @@ def parse(argv=None):
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    ap.add_argument("--rebuilds", type=int, default=3, help="warm rebuilds timed for build_ms (median)")
+    ap.add_argument("--rebuilds", type=int, default=5, help="warm rebuilds timed for build_ms (median)")
     ap.add_argument("--spawn-check", action="store_true", help=argparse.SUPPRESS)  # tests: report ranks and exit
     return ap.parse_args(argv)
 
@@ -448,7 +448,8 @@ def run_ours(a):
             "warmup": a.warmup, "ms_per_step": round(ms / a.steps, 4), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": C["dtype"], "data": "synthetic (seeded generators, DESIGN.md Workloads)",
             "config": config_dict(a, w, grid.max_level, world),
-            "index": {"layout": layout, "root_level": st["root_level"], "index_bytes": st["index_bytes"],
+            "index": {"layout": layout, "search": SEARCH.get(layout), "root_level": st["root_level"],
+                      "index_bytes": st["index_bytes"],
                       "boundary_leaves": st["n_boundary_cells"],
                       "n_nodes": st["n_nodes"], "hot_regions": None if prep.index._hot is None else len(prep.index._hot),
                       "build_ms": round(float(np.median(warm_ms)), 1) if warm_ms else None,
@@ -460,6 +461,16 @@ def run_ours(a):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+# how each layout resolves a point's 64-bit leaf cell key (Z code) to its covering cell
+SEARCH = {
+    "trie": "radix search over the 64-bit leaf keys: root slot = top 2*T0 key bits, each node level the next "
+            "2k bits, coarse cells expanded into the slots they cover (one dependent read per level)",
+    "packed": "the radix search with its last level as 16-byte palette blocks of 4x4 leaves",
+    "keys": "sorted 64-bit cell-key records, a radix table over the top key bits, then binary search in the bucket",
+    "dense": "one slot per leaf (uniform raster)",
+}
 
 
 def run_reference(a):

@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -383,6 +384,11 @@ struct rb_approx {
   int pd = 0;
   rb::DBuf hot_region;  // int32 [n_hot]: hot slot -> region
   int32_t n_hot = 0;
+  // partitioned point pass (rb_binned.cuh): per level-bin_level cell, whether any root slot below it is set
+  // (points in uncovered bins have no owner); computed on first use
+  rb::DBuf bin_flags;
+  int bin_level = -1, bin_used = 0;
+  std::mutex bin_mu;
   // Owner codes ((region << 1) | boundary) + 1 take code_bits = bit length of 2 * n_regions (<= 18); the hot
   // slot annotation (slot + 1) sits above them, up to bit 29: 2^(30 - code_bits) - 1 slots (4095 .. 16383)
   uint32_t code_mask = RB_CODE_MASK, hot_shift = RB_HOT_SHIFT;
@@ -404,8 +410,8 @@ struct rb_approx {
   rb_stats stats{};
   // buffers kept past the build no longer belong to the build stream
   void detach_all() {
-    for (rb::DBuf* b : {&root, &pool, &summary, &keys, &ktab, &pblk, &pwide, &hot_region, &cell_poly, &cell_level,
-                        &cell_code, &cell_kind, &part_poly, &part_code, &part_kept})
+    for (rb::DBuf* b : {&root, &pool, &summary, &keys, &ktab, &pblk, &pwide, &hot_region, &bin_flags, &cell_poly,
+                        &cell_level, &cell_code, &cell_kind, &part_poly, &part_code, &part_kept})
       b->detach();
     for (auto& b : node_bufs) b.detach();
   }

@@ -2230,6 +2230,8 @@ static cudaError_t deep_dispatch(int ci, const PassArgs& a, size_t smem, cudaStr
   }
 }
 
+#include "rb_binned.cuh"
+
 #define RB_DISPATCH_TMA(FN, GHV, ...)                                                          \
   (dtype == RB_XY_F64 ? (attr ? FN<0, true, GHV>(__VA_ARGS__) : FN<0, false, GHV>(__VA_ARGS__)) \
                       : (attr ? FN<1, true, GHV>(__VA_ARGS__) : FN<1, false, GHV>(__VA_ARGS__)))
@@ -2329,6 +2331,14 @@ int point_pass(const rb_approx* A, const void* xy, int32_t dtype, int64_t n, con
     if (tstart()) return RB_CUDA_ERROR;
     e = dtype == RB_XY_F64 ? launch_a<0, false>(a, vec, blocks, 0, s) : launch_a<1, false>(a, vec, blocks, 0, s);
     if (e) return cuda_fail(e, "k_point_pass_global");
+    return tstop();
+  }
+  // partitioned pass (rb_binned.cuh): large batches on the radix table with region sets beyond shared memory
+  if (g_kernel_sel != 0 && g_kernel_sel != 3 && g_kernel_sel != 4 && binned_wanted(A, n, aligned, smem_hist)) {
+    if (tstart()) return RB_CUDA_ERROR;
+    int nl = 0;
+    if (int st = binned_pass(A, a, dtype, attr != nullptr, s, &nl)) return st;
+    g_launches += nl - 1;  // tstop counts one
     return tstop();
   }
   int blocks = 0;
