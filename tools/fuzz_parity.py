@@ -1,6 +1,6 @@
 """Randomised parity against the oracle: random (possibly overlapping, holed)
 polygons, random grid levels, both modes, every index layout (radix table, sorted keys, dense grid, packed
-in both forms), f64/f32
+in both forms) and the opt-in partitioned pass, f64/f32
 points drawn uniformly, clustered, on grid lines and on polygon vertices,
 attributes spanning many magnitudes (zero, negative, out of the fixed-point
 window).  COUNT must be bit-exact, SUM within rel 1e-6.  Prints one line per
@@ -40,8 +40,9 @@ for c in range(cases):
         regions = random_polygons(int(seed0 + c), int(rng.integers(3, 40)), holes=(kind == "holes"))
         L = int(rng.integers(3, 22))  # up to 21: beyond the ring kernels' 2^20 window
     mode = int(rng.integers(0, 2))
-    layouts = [("trie", -1), ("keys", -1), ("packed", -1)] + ([("packed", L - 3)] if 3 <= L <= 19 else []) + \
-        ([("dense", -1)] if L <= 12 else [])
+    # "binned": the radix table through the opt-in partitioned pass (RB_BINNED=1, csrc/rb_binned.cuh)
+    layouts = [("trie", -1), ("binned", -1), ("keys", -1), ("packed", -1)] + \
+        ([("packed", L - 3)] if 3 <= L <= 19 else []) + ([("dense", -1)] if L <= 12 else [])
     grid = GridConfig(Point2D(0.0, 0.0), 1.0, L)
     n = int(rng.integers(1, 300_000))
     parts = [rng.random((n, 2))]
@@ -62,7 +63,8 @@ for c in range(cases):
     if kind == "big" and rng.random() < 0.5:  # an explicit hot subset: cold regions take the global REDs
         hot = np.sort(rng.choice(p.n_regions, int(rng.integers(0, min(4095, p.n_regions))), replace=False))
     for layout, rl in layouts:
-        idx = ApproxIndex(p, grid, mode, layout=layout, root_level=rl)
+        idx = ApproxIndex(p, grid, mode, layout="trie" if layout == "binned" else layout, root_level=rl)
+        os.environ["RB_BINNED"] = "1" if layout == "binned" else "0"
         if hot is not None:
             idx.set_hot(hot)
         for pts, at in ((xy, attr), (xy.astype(np.float32), None)):
@@ -83,6 +85,7 @@ for c in range(cases):
                       f"n={len(pts)} f32={pts.dtype == np.float32} count_diff={int(np.abs(cnt - cnt_o).sum())}",
                       flush=True)
         del idx
+    os.environ.pop("RB_BINNED", None)
     print(f"case {c}: {kind} R={p.n_regions} L={L} mode={mode} n={len(xy)} layouts={[x for x, _ in layouts]} ok",
           flush=True)
 print(f"{cases} cases, {fails} mismatches, {time.time() - t0:.0f} s")

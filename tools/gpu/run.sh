@@ -1,2 +1,2 @@
-timeout 300 python tools/profile_pass.py c4 200000000 packed 1 > gpurun_out/plain_pp_c4_packed.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_point_pass -s 1 -c 1 -o gpurun_out/prof_c4_pkl python tools/profile_pass.py c4 200000000 packed 1 > gpurun_out/ncu_full_c4_pkl.log 2>&1; echo rc=$?
+timeout 3000 python tools/fuzz_parity.py 200 70000 > gpurun_out/r2_fuzz5.log 2>&1; echo fuzz5 rc=$?
+timeout 3000 python tools/fuzz_parity.py 60 80000 big > gpurun_out/r2_fuzz6.log 2>&1; echo fuzz6 rc=$?
