@@ -24,10 +24,11 @@
 //                           into the outputs at the end of the item.
 //
 // Measured (B200, C4 at 100M points, ncu launch times): pass 1 1.84 ms, plan 0.08 ms, pass 2 1.21 ms
-// against 0.83 ms for k_point_pass_deep (profiles/round2/binned_experiment.txt).  Even at its bounds -- pass 1
-// HBM-bound on 20 B/pt, pass 2 on 8 B/pt -- the two passes would take ~0.65 ms, so the extra 16 B/pt of
-// traffic caps the gain at ~1.28x; the first cut is issue-bound (pass 1: 175 instructions per point and a
-// global chunk-allocation atomic per tile; pass 2: a shared hash probe per point).  It stays an opt-in
+// against 0.83 ms for k_point_pass_deep (profiles/round2/binned_experiment.txt).  At the HBM rate the ring
+// kernel sustains (4.8 TB/s) the two passes' 28 B/pt would take 0.58 ms per 100M points (1.4x), but only
+// if both ran near that rate: pass 2 streams 8 B/pt, so it would have to spend <= ~40 instructions per point
+// at the achieved IPC, against 147 in the one-pass kernel; the first cut spends 175 (pass 1: plus a global
+// chunk-allocation atomic per tile) and 210 (pass 2: a shared hash probe per point).  It stays an opt-in
 // experiment (RB_BINNED=1), parity-tested; the one-pass deep kernel remains the C4 path.
 //
 // The index, the quantisation and the owner semantics are those of the one-pass kernels, so COUNT is

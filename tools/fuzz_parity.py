@@ -30,13 +30,17 @@ t0 = time.time()
 for c in range(cases):
     rng = np.random.default_rng(seed0 + c)
     kind = rng.choice(["random", "holes", "tiling", "big"]) if len(sys.argv) <= 3 else sys.argv[3]
-    if kind == "tiling":
-        regions = W.voronoi_tiling(int(rng.integers(20, 400)), 1.0, seed=int(seed0 + c), verts=(6, 20))
-        L = int(rng.integers(3, 15))
-    elif kind == "big":  # region sets beyond shared memory: deep / global kernels, hot slots
-        regions = W.voronoi_tiling(int(rng.integers(2000, 6000)), 1.0, seed=int(seed0 + c), verts=(6, 14))
-        L = int(rng.integers(10, 15))
-    else:
+    try:
+        if kind == "tiling":
+            regions = W.voronoi_tiling(int(rng.integers(20, 400)), 1.0, seed=int(seed0 + c), verts=(6, 20))
+            L = int(rng.integers(3, 15))
+        elif kind == "big":  # region sets beyond shared memory: deep / global kernels, hot slots
+            regions = W.voronoi_tiling(int(rng.integers(2000, 6000)), 1.0, seed=int(seed0 + c), verts=(6, 14))
+            L = int(rng.integers(10, 15))
+    except RuntimeError as e:  # the tiling generator gave up on this seed (no simple polygons): not a parity case
+        print(f"case {c}: {kind} skipped ({e})", flush=True)
+        continue
+    if kind in ("random", "holes"):
         regions = random_polygons(int(seed0 + c), int(rng.integers(3, 40)), holes=(kind == "holes"))
         L = int(rng.integers(3, 22))  # up to 21: beyond the ring kernels' 2^20 window
     mode = int(rng.integers(0, 2))
