@@ -1466,7 +1466,7 @@ __device__ __forceinline__ void redg_sum(double* p, double w, bool pred) {
                : "memory");
 }
 
-// ABL (timing experiments only, RB_DEEP_ABLATE; results are wrong): 1 = drop cold-region REDs,
+// ABL (timing experiments only, RB_DEEP_ABLATE; results are wrong): 1 = drop cold-region REDs (LAY 0 and 2),
 // 2 = no palette-block loads (every point of a mixed root cell counts as hot slot 0), 4 = no root loads
 template <int XY, bool ATTR, int NW, int PPT, int NST, int LAY = 0, int ABL = 0>
 __global__ void __launch_bounds__(NW * 32 + 32, 1) k_point_pass_deep(PassArgs a) {
@@ -2203,14 +2203,14 @@ static const WarpCfg kDeepCfgs[] = {{16, 4, 3}, {16, 4, 2}, {16, 4, 4}, {15, 4, 
 
 template <int XY, bool ATTR, int LAY = 0>
 static cudaError_t deep_dispatch(int ci, const PassArgs& a, size_t smem, cudaStream_t s, int* blocks, bool launch) {
-  if constexpr (XY == 1 && ATTR && LAY == 2) {  // timing ablations of the C4 kernel (tools/, RB_DEEP_ABLATE)
+  if constexpr (XY == 1 && ATTR && (LAY == 2 || LAY == 0)) {  // timing ablations of the C4 kernel (tools/, RB_DEEP_ABLATE)
     static int abl = -1;
     if (abl < 0) { const char* e = getenv("RB_DEEP_ABLATE"); abl = e ? atoi(e) : 0; }
     switch (abl) {
       case 1: return deep_run<XY, ATTR, 16, 4, 3, LAY, 1>(a, smem, s, blocks, launch);
-      case 3: return deep_run<XY, ATTR, 16, 4, 3, LAY, 3>(a, smem, s, blocks, launch);
-      case 7: return deep_run<XY, ATTR, 16, 4, 3, LAY, 7>(a, smem, s, blocks, launch);
-      case 6: return deep_run<XY, ATTR, 16, 4, 3, LAY, 6>(a, smem, s, blocks, launch);
+      case 3: if constexpr (LAY == 2) return deep_run<XY, ATTR, 16, 4, 3, LAY, 3>(a, smem, s, blocks, launch); break;
+      case 7: if constexpr (LAY == 2) return deep_run<XY, ATTR, 16, 4, 3, LAY, 7>(a, smem, s, blocks, launch); break;
+      case 6: if constexpr (LAY == 2) return deep_run<XY, ATTR, 16, 4, 3, LAY, 6>(a, smem, s, blocks, launch); break;
       default: break;
     }
   }

@@ -1,2 +1,5 @@
-timeout 3500 python tools/fuzz_parity.py 600 90000 > gpurun_out/r2_fuzz7.log 2>&1; echo fuzz7 rc=$?
-timeout 2000 python tools/fuzz_parity.py 100 95000 big > gpurun_out/r2_fuzz8.log 2>&1; echo fuzz8 rc=$?
+for r in 1 2; do
+  for ab in 0 1; do
+    RB_DEEP_ABLATE=$ab timeout 300 python tools/profile_pass.py c4 200000000 trie 3 2>&1 | grep Gpts | tail -1 | sed "s|^|ablate=$ab |"
+  done
+done
