@@ -88,7 +88,7 @@ __global__ void k_bin_flags(const uint32_t* __restrict__ root, int T0, int BL, i
 template <int XY, bool ATTR>
 __global__ void __launch_bounds__(binned::P1_NT, 2) k_bin_scatter(BinArgs b) {
   using namespace binned;
-  extern __shared__ __align__(16) unsigned char sm[];
+  extern __shared__ __align__(128) unsigned char sm[];
   const int NB = 1 << (2 * b.BL);
   uint32_t* hc = (uint32_t*)sm;          // [NB + 1]: tile counts, then exclusive offsets (hc[NB] = tile total)
   uint32_t* scur = hc + NBMAX + 4;       // open chunk per bin (NONE: none yet)

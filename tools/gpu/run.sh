@@ -1,5 +1,5 @@
-for r in 1 2; do
-  for ab in 0 1; do
-    RB_DEEP_ABLATE=$ab timeout 300 python tools/profile_pass.py c4 200000000 trie 3 2>&1 | grep Gpts | tail -1 | sed "s|^|ablate=$ab |"
+for r in 1 2 3; do
+  for lib in build/ab/lib_base.so build/ab/lib_u2.so; do
+    RASTERBOUND_B200_LIB=$lib timeout 300 python tools/profile_pass.py c2 100000000 trie 5 2>&1 | grep Gpts | tail -1 | sed "s|^|$lib |"
   done
 done
