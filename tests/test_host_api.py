@@ -278,3 +278,22 @@ def test_eps_grid_leaf_side_is_eps_over_sqrt2():
         assert g.extent >= 1.02 * span and g.extent / 2 < 1.02 * span
         assert level_for_bound(g, eps) == g.max_level
     assert eps_grid(0.0, 0.0, 100_000.0, 100_000.0, 1.0).max_level == 18
+
+
+def test_integration_stub_structs_match_the_binding():
+    """INTEGRATION.md section B's ctypes structs have the layout of the header's
+    (as bound by _native.py); the block executes as written (library path filled in)."""
+    import re
+
+    from paper_2010_12548_b200 import _native as N
+
+    text = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    code = re.search(r"```python\n(.*?)```", text[text.index("## B."):], re.S).group(1)
+    lib = os.path.join(ROOT, "paper_2010_12548_b200", "lib", "librasterbound_b200.so")
+    ns = {}
+    exec(compile(code.replace('C.CDLL("librasterbound_b200.so")', f"C.CDLL({lib!r})"), "INTEGRATION.md#B", "exec"), ns)
+    for stub, ours in (("rb_grid", N.Grid), ("rb_polygons", N.Polygons), ("rb_build_opts", N.BuildOpts)):
+        s = ns[stub]
+        assert ctypes.sizeof(s) == ctypes.sizeof(ours), stub
+        assert [f[0] for f in s._fields_] == [f[0] for f in ours._fields_], stub
+        assert [getattr(s, f[0]).offset for f in s._fields_] == [getattr(ours, f[0]).offset for f in ours._fields_]
