@@ -1,1 +1,1 @@
-timeout 600 python -m pytest tests/test_gpu_integration_stub.py tests/test_gpu_capacity.py -q -x 2>&1 | tail -3
+timeout 600 python bench.py --config c1 --steps 5 --warmup 3 > gpurun_out/bench_c1.json 2> gpurun_out/bench_c1.err; echo rc=$?; tail -c 400 gpurun_out/bench_c1.json
