@@ -71,6 +71,23 @@ def parse(argv=None):
     return ap.parse_args(argv)
 
 
+def clear_cuda_error():
+    """Reset the CUDA runtime's last-error state (torch's dynamic libcudart; torch does not expose it)."""
+    import ctypes
+    import glob
+
+    import torch
+
+    cands = ["libcudart.so.12"] + glob.glob(os.path.join(os.path.dirname(torch.__file__), "..", "nvidia", "cuda_runtime",
+                                                         "lib", "libcudart.so*"))
+    for name in cands:
+        try:
+            ctypes.CDLL(name).cudaGetLastError()
+            return
+        except (OSError, AttributeError):
+            continue
+
+
 def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
@@ -366,8 +383,12 @@ def run_ours(a):
         cudart = torch.cuda.cudart()
         pinned = []
         for arr in (w.xy, attr_np):
-            if arr is not None and int(cudart.cudaHostRegister(arr.ctypes.data, arr.nbytes, 0)) == 0:
+            if arr is None:
+                continue
+            if int(cudart.cudaHostRegister(arr.ctypes.data, arr.nbytes, 0)) == 0:
                 pinned.append(arr)
+            else:
+                clear_cuda_error()  # a failed registration must not surface in torch's next launch check
         xy_pin = torch.from_numpy(w.xy)
         at_pin = torch.from_numpy(attr_np) if attr_np is not None else None
 
