@@ -1,5 +1,4 @@
-for r in 1 2; do
-  for ab in 0 1 8; do
-    RB_DEEP_ABLATE=$ab timeout 300 python tools/profile_pass.py c4 200000000 trie 3 2>&1 | grep Gpts | tail -1 | sed "s|^|ablate=$ab |"
-  done
-done
+# scratch command file for gpurun calls; the last one: the full GPU suite, the default bench line and smoke()
+timeout 2400 python -m pytest tests -m gpu -q -p no:cacheprovider 2>&1 | tail -2
+timeout 900 python bench.py > gpurun_out/bench_c4_final.json 2> gpurun_out/bench_c4_final.err; echo bench rc=$?
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" 2>&1 | tail -1
